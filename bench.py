@@ -1,0 +1,407 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the batched HPD inversion hot path (BASELINE.json metric).
+
+One step = one pass of the whole hot path (load upper(A) -> Cholesky/LDL -> proposed
+inversion -> mirror -> store) over one batch of synthetic matrices, i.e.
+one call of the C ABI entry point.  Default workload: BASELINE.json configs[1] (cfg2: 2^20
+complex64 8x8 HPD matrices, interleaved layout) on N=1 GPU.  `--config k` selects another.
+
+Multi-GPU (torchrun, one process per GPU): every rank inverts its own slice of a global
+batch of N x B matrices generated locally from chunk-keyed seeds (weak scaling, no data-path
+collective).  Timing: CUDA events on the launching stream between a barrier +
+synchronize on both sides; the max over ranks is reported.
+
+`--impl reference` times the fp64 CPU oracle (the reference arm of this tier) on bounded
+samples of the same workload, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1111_4144_b200 import workloads as wl  # noqa: E402
+
+METRIC = "HPD matrices inverted/sec (N=8,16,64) and % of HBM/FP roofline, 1-8 B200"
+UNIT = "matrices/s"
+L2_BYTES = 126 * 2**20
+SMS = 148
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=None)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", type=int, default=2, choices=sorted(wl.CONFIGS))
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def algorithmic_bytes(cfg: wl.Config) -> int:
+    """Per matrix: read the upper triangle, write all n^2 entries of X and one int32 info."""
+    n, e = cfg.n, cfg.elem_bytes
+    return e * (n * (n + 1) // 2 + n * n) + 4
+
+
+def cmul_per_matrix(n: int) -> int:
+    return (n ** 3 - n) // 2          # Table 1 proposed total, exact
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        mp = json.load(open(path))
+        return {"hbm_gbs": float(mp["hbm_gbs"]), "sm_max_mhz": float(mp.get("sm_max_mhz", 1965.0)),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def fp_peak_tflops(dtype: torch.dtype, mhz: float) -> float:
+    """FP32 / FP64 FMA peak from unit counts: 148 SMs x {128, 64} FMA/clk x 2."""
+    lanes = 128 if dtype == torch.complex64 else 64
+    return SMS * lanes * 2 * mhz * 1e6 / 1e12
+
+
+class ClockSampler:
+    """Samples SM clock and clock-event reasons via NVML while the timed region runs."""
+    NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+             0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+             0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+             0x100: "display_clock_setting"}
+
+    def __init__(self, cuda_device: int, period_s: float = 0.005):
+        self.samples = []
+        self.period = period_s
+        self.ok = False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            pr = torch.cuda.get_device_properties(cuda_device)
+            try:
+                bus = "%08X:%02X:%02X.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(cuda_device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - depends on the box
+            self.err = repr(e)
+            self.max_mhz = None
+
+    def _sample(self):
+        nv = self.nv
+        try:
+            mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+            try:
+                reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                reasons = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+            self.samples.append((mhz, int(reasons)))
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self._stop.is_set():
+            self._sample()
+            time.sleep(self.period)
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self.ok:
+            self._sample()
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0,
+                    "note": getattr(self, "err", "no samples")}
+        mhz = [s[0] for s in self.samples]
+        mask = 0
+        for s in self.samples:
+            mask |= s[1]
+        reasons = [v for k, v in self.NAMES.items() if mask & k and k != 0x1]
+        return {"sm_mhz": float(statistics.median(mhz)), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def load_traffic(cfg: wl.Config, kernel: str):
+    """Per-launch DRAM bytes of this kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        t = json.load(open(path))
+        rec = t.get("cfg%d" % cfg.cid)
+        if rec and rec.get("kernel") == kernel and rec.get("batch") == cfg.batch:
+            return float(rec["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
+
+
+# ------------------------------------------------------------------------------ ours
+def run_ours(args, rank, world, local_rank):
+    import paper_1111_4144_b200 as hp
+
+    cfg = wl.CONFIGS[args.config]
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    B = cfg.batch
+    A = wl.generate(cfg, rank * B, B, device=dev, seed=args.seed)   # this rank's slice
+    store, view = wl.to_layout(A, cfg.layout)
+    del A
+    X = wl.empty_like_layout(view)
+    info = torch.empty(B, dtype=torch.int32, device=dev)
+    kernel = hp.kernel_name(cfg.method, cfg.dtype, B, cfg.n, (view.stride(0), view.stride(2)))
+
+    def step():
+        hp.invert(view, cfg.method, X=X, info=info)
+
+    per_step_guess = algorithmic_bytes(cfg) * B / 6.0e12
+    steps = args.steps if args.steps is not None else max(20, min(2000, int(0.5 / per_step_guess)))
+    warmup = max(3, args.warmup)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier(device_ids=[local_rank])
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    bad = int((info != 0).sum().item())
+    barrier()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    sampler.start()
+    t0.record(stream)
+    for k in range(steps):
+        evs[k][0].record(stream)
+        step()
+        evs[k][1].record(stream)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    sampler.stop()
+    barrier()
+    elapsed_ms = t0.elapsed_time(t1)
+    kern_ms = sum(a.elapsed_time(b) for a, b in evs) / steps
+    t = torch.tensor([elapsed_ms, kern_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    elapsed_ms, kern_ms = t.tolist()
+    ms_per_step = elapsed_ms / steps
+    value = world * B / (ms_per_step / 1e3)
+
+    # ---- end to end through the host-buffer C entry point (H2D + kernel + D2H timed)
+    e2e = None
+    if not args.no_e2e:
+        A_host = store.cpu().pin_memory()
+        if cfg.layout == "soa":
+            vh = wl.soa_view(A_host, B, cfg.n)
+            X_host = torch.empty_like(A_host).pin_memory()
+            xh = wl.soa_view(X_host, B, cfg.n)
+            h2d = cfg.elem_bytes * cfg.n * (cfg.n + 1) // 2 * B
+        else:
+            vh = A_host
+            X_host = torch.empty_like(A_host).pin_memory()
+            xh = X_host
+            h2d = cfg.elem_bytes * cfg.n * cfg.n * B
+        info_h = torch.empty(B, dtype=torch.int32).pin_memory()
+        chunk = max(4096, B // 8)
+        ws = torch.empty(hp.host_workspace_bytes(cfg.dtype, cfg.n, chunk), dtype=torch.uint8, device=dev)
+        e2e_steps = max(3, min(steps, 10))
+        for _ in range(2):
+            hp.invert_host(vh, cfg.method, xh, info_h, ws, chunk)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(e2e_steps):
+            hp.invert_host(vh, cfg.method, xh, info_h, ws, chunk)
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        te = torch.tensor([a.elapsed_time(b) / e2e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        # the result read back must match the device-resident run bit for bit
+        same = torch.equal(xh.contiguous(), X.cpu().contiguous()) and torch.equal(info_h, info.cpu())
+        e2e = {"value": world * B / (te.item() / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(cfg.elem_bytes * cfg.n * cfg.n * B + 4 * B),
+               "ms_per_step": te.item(), "chunk": chunk, "matches_device_run": bool(same),
+               "api": "hpdinv_inv_host (pinned host buffers)"}
+
+    # ---- roofline of the (single) kernel of the step
+    pk = peaks()
+    clocks = sampler.summary()
+    bytes_launch = algorithmic_bytes(cfg) * B
+    mem_s = bytes_launch / (pk["hbm_gbs"] * 1e9)
+    fp_tf = fp_peak_tflops(cfg.dtype, pk["sm_max_mhz"])
+    flops_launch = 8.0 * cmul_per_matrix(cfg.n) * B
+    fp_s = flops_launch / (fp_tf * 1e12)
+    if fp_s > mem_s:
+        achieved = flops_launch / (kern_ms / 1e3) / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": fp_tf, "unit": "TFLOP/s",
+                "frac": achieved / fp_tf, "peak_source": "derived: 148 SMs x %d FMA/clk x 2 x %.0f MHz"
+                % (128 if cfg.dtype == torch.complex64 else 64, pk["sm_max_mhz"])}
+    else:
+        achieved = bytes_launch / (kern_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "peak_source": pk["source"]}
+    roof["traffic"] = load_traffic(cfg, kernel)
+    roof["algorithmic_bytes_per_launch"] = bytes_launch
+    roof["kernel"] = kernel
+    roof["kernel_ms"] = kern_ms
+    # BASELINE.json's own formula: max(16 N^2 batch / HBM, multiply count / FP peak)
+    bj_bytes = 2 * cfg.elem_bytes * cfg.n ** 2 * B
+    bj_t = max(bj_bytes / (pk["hbm_gbs"] * 1e9), fp_s)
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if cfg.dtype == torch.complex64 else "f64",
+        "data": "synthetic (seeded, chunk-keyed; BASELINE.json configs recipe)",
+        "config": {"workload": "cfg%d: %s" % (cfg.cid, cfg.desc), "n": cfg.n,
+                   "batch_per_gpu": B, "global_batch": world * B,
+                   "elem": "complex64" if cfg.dtype == torch.complex64 else "complex128",
+                   "method": cfg.method, "layout": cfg.layout,
+                   "parallelism": "batch slices, %d rank(s), no collective" % world,
+                   "l2": "inputs larger than L2 (%.0f MB working set > 126 MB); no flush"
+                   % ((bj_bytes) / 1e6) if bj_bytes > L2_BYTES else "working set fits L2"},
+        "roofline": roof,
+        "roofline_baseline_formula": {"time_s": bj_t, "frac": bj_t / (kern_ms / 1e3),
+                                      "bytes": bj_bytes, "note": "BASELINE.json north_star formula"},
+        "clocks": clocks, "gpu_launches": steps, "info_nonzero": bad, "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg, args, budget_s=args.cpu_seconds, dev=dev)
+    return out
+
+
+# ------------------------------------------------------------------- the oracle arm
+def oracle_sample(cfg: wl.Config, count: int, seed: int, dev):
+    """Host complex128 copy of the first `count` matrices of the workload (exact upcast of
+    the bits the GPU consumes when generated on the GPU)."""
+    A = wl.generate(cfg, 0, count, device=dev, seed=seed)
+    return A.cpu().to(torch.complex128).numpy()
+
+
+def cpu_baseline(cfg: wl.Config, args, budget_s: float, dev):
+    import oracle
+    oracle.build()
+    cores = oracle.max_threads()
+    Ah = oracle_sample(cfg, min(cfg.batch, 1024), args.seed, dev)
+    t0 = time.perf_counter()
+    oracle.inv_batched(Ah, cfg.method)
+    per = (time.perf_counter() - t0) / Ah.shape[0]
+    count = int(min(cfg.batch, max(Ah.shape[0], budget_s / max(per, 1e-9))))
+    Ah = oracle_sample(cfg, count, args.seed, dev)
+    t0 = time.perf_counter()
+    oracle.inv_batched(Ah, cfg.method)
+    dt = time.perf_counter() - t0
+    return {"value": count / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": "first %d of the %d matrices of cfg%d (%s), fp64 C oracle, OpenMP over matrices"
+            % (count, cfg.batch, cfg.cid, cfg.method), "seconds": dt,
+            "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args, rank, world):
+    import oracle
+    oracle.build()
+    cfg = wl.CONFIGS[args.config]
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+    steps = args.steps if args.steps is not None else 5
+    warmup = args.warmup if args.warmup is not None else 1
+    # each step: a bounded sample sized so the whole run takes ~2-3 minutes
+    Ah = oracle_sample(cfg, min(cfg.batch, 512), args.seed, dev)
+    t0 = time.perf_counter()
+    oracle.inv_batched(Ah, cfg.method)
+    per = (time.perf_counter() - t0) / Ah.shape[0]
+    per_step_s = max(0.2, min(20.0, 150.0 / max(1, steps + warmup)))
+    count = int(min(cfg.batch, max(64, per_step_s / max(per, 1e-9))))
+    Ah = oracle_sample(cfg, count, args.seed, dev)
+    for _ in range(warmup):
+        oracle.inv_batched(Ah, cfg.method)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        X, info = oracle.inv_batched(Ah, cfg.method)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = count / (ms / 1e3)
+    cores = oracle.max_threads()
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": steps, "warmup": warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg%d: %s" % (cfg.cid, cfg.desc), "n": cfg.n,
+                   "batch_per_gpu": cfg.batch, "method": cfg.method, "layout": cfg.layout,
+                   "sample_per_step": count},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": "first %d of the %d matrices of cfg%d per step" % (count, cfg.batch, cfg.cid),
+                         "cpu": _cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "info_nonzero": int((info != 0).sum()),
+    }
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        print(json.dumps(run_reference(args, rank, world)), flush=True)
+        return 0
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,51 @@
+"""ctypes loader for the in-tree libhpdinv.so (include/hpdinv.h).  Fails loudly if the CUDA
+library has not been built: there is no CPU fallback anywhere in the product path."""
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhpdinv.so")
+
+_lib = None
+
+
+class HpdinvError(RuntimeError):
+    pass
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise HpdinvError(
+            "libhpdinv.so is not built (%s). Run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "or `python paper_1111_4144_b200/_build.py`." % LIB_PATH)
+    L = ctypes.CDLL(LIB_PATH)
+    P, I, I64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+    inv_args = [I64, I, P, I64, I64, P, I64, I64, P, P]
+    for name in ("chol_inv_batched_c64", "chol_inv_batched_c128",
+                 "ldl_inv_batched_c64", "ldl_inv_batched_c128"):
+        f = getattr(L, name)
+        f.restype = I
+        f.argtypes = inv_args
+    L.hpdinv_host_workspace_bytes.restype = ctypes.c_size_t
+    L.hpdinv_host_workspace_bytes.argtypes = [I, I, I64]
+    L.hpdinv_inv_host.restype = I
+    L.hpdinv_inv_host.argtypes = [I, I, I64, I, P, I64, I64, P, I64, I64, P, P, ctypes.c_size_t,
+                                  I64, P]
+    L.hpdinv_kernel_name.restype = ctypes.c_char_p
+    L.hpdinv_kernel_name.argtypes = [I, I, I64, I, I64, I64, I64, I64]
+    L.hpdinv_version.restype = ctypes.c_char_p
+    L.hpdinv_version.argtypes = []
+    _lib = L
+    return L
+
+
+# Every symbol include/hpdinv.h declares (checked by tests/test_abi.py without a GPU).
+EXPORTS = (
+    "chol_inv_batched_c64", "chol_inv_batched_c128",
+    "ldl_inv_batched_c64", "ldl_inv_batched_c128",
+    "hpdinv_host_workspace_bytes", "hpdinv_inv_host",
+    "hpdinv_kernel_name", "hpdinv_version",
+)

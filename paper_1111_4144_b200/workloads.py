@@ -1,0 +1,142 @@
+"""Seeded synthetic inputs shaped like BASELINE.json's configs (shared by tests, bench and
+smoke).  This module holds NONE of the method's arithmetic: it only draws random matrices
+and lays them out in memory.  Both the CUDA path and the oracle consume the same bits.
+
+Recipe (BASELINE.json "configs"):
+  cfg1  N=4   c64   1024   Cholesky  SoA   A = B B^H / 4  + 0.1 I
+  cfg2  N=8   c64   2^20   Cholesky  SoA   A = B B^H / 8  + 0.1 I   ("interleaved")
+  cfg3  N=16  c64   2^22   Cholesky  SoA   A = B B^H / 16 + 0.01 I  (reading R15)
+  cfg4  N=64  c128  2^18   Cholesky  AoS   A = Q diag(lam) Q^H, Q from QR of CN(0,1),
+                                           lam = 10^(3U), U ~ U[0,1) (log-uniform [1,1e3])
+  cfg5  N=32  c64   2^20   LDL       AoS   A = B B^H / 32 + 0.05 I
+B has i.i.d. CN(0,1) entries (re, im each N(0, 1/2): torch complex randn).  A is made
+exactly Hermitian as (A + A^H)/2 with Im a_ii = 0.  Matrices are drawn in chunks of
+CHUNK; chunk c of config k uses its own generator seeded from (seed, k, c), so any slice
+[start, start+count) of the global batch -- e.g. one rank's shard -- is generated
+independently and bit-identically to the same slice of an unsharded run (same device type).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import torch
+
+CHUNK = 4096
+
+
+@dataclass(frozen=True)
+class Config:
+    cid: int
+    n: int
+    dtype: torch.dtype
+    batch: int
+    method: str            # "chol" | "ldl"
+    layout: str            # "soa" | "aos"
+    kind: str              # "bbh" | "spectral"
+    divisor: float = 1.0   # A = B B^H / divisor + delta I
+    delta: float = 0.0
+    desc: str = ""
+
+    @property
+    def elem_bytes(self) -> int:
+        return 8 if self.dtype == torch.complex64 else 16
+
+
+CONFIGS = {
+    1: Config(1, 4, torch.complex64, 1024, "chol", "soa", "bbh", 4.0, 0.1,
+              "1024 c64 HPD 4x4, A = BB^H/4 + 0.1I, Cholesky + proposed, seed 0"),
+    2: Config(2, 8, torch.complex64, 1 << 20, "chol", "soa", "bbh", 8.0, 0.1,
+              "2^20 c64 HPD 8x8, A = BB^H/8 + 0.1I, interleaved (SoA) batch layout"),
+    3: Config(3, 16, torch.complex64, 1 << 22, "chol", "soa", "bbh", 16.0, 0.01,
+              "2^22 c64 HPD 16x16, A = BB^H/16 + 0.01I, interleaved (SoA)"),
+    4: Config(4, 64, torch.complex128, 1 << 18, "chol", "aos", "spectral", 1.0, 0.0,
+              "2^18 c128 HPD 64x64, A = Q diag(lam) Q^H, lam log-uniform [1,1e3], one matrix per CTA"),
+    5: Config(5, 32, torch.complex64, 1 << 20, "ldl", "aos", "bbh", 32.0, 0.05,
+              "2^20 c64 HPD 32x32, A = BB^H/32 + 0.05I, LDL R*DR + proposed"),
+}
+
+
+def chunk_seed(seed: int, cid: int, chunk: int) -> int:
+    # splitmix64-style mixing of (seed, config, chunk) into a 63-bit torch seed
+    x = (seed * 0x9E3779B97F4A7C15 + cid * 0xBF58476D1CE4E5B9 + chunk * 0x94D049BB133111EB) & (2**64 - 1)
+    x ^= x >> 31
+    x = (x * 0xD6E8EB7A8B3F7C5B) & (2**64 - 1)
+    x ^= x >> 29
+    return x & (2**63 - 1)
+
+
+def _hermitise(A: torch.Tensor) -> torch.Tensor:
+    A = (A + A.conj().transpose(-1, -2)) * 0.5
+    d = torch.diagonal(A, dim1=-2, dim2=-1)
+    d.imag.zero_()
+    return A
+
+
+def _gen_chunk(cfg: Config, chunk: int, count: int, device, seed: int) -> torch.Tensor:
+    g = torch.Generator(device=device)
+    g.manual_seed(chunk_seed(seed, cfg.cid, chunk))
+    n = cfg.n
+    if cfg.kind == "bbh":
+        B = torch.randn(count, n, n, dtype=cfg.dtype, device=device, generator=g)
+        A = torch.matmul(B, B.conj().transpose(-1, -2)) / cfg.divisor
+        A = A + cfg.delta * torch.eye(n, dtype=cfg.dtype, device=device)
+        return _hermitise(A)
+    # spectral: A = Q diag(lam) Q^H
+    G = torch.randn(count, n, n, dtype=cfg.dtype, device=device, generator=g)
+    U = torch.rand(count, n, dtype=torch.float64, device=device, generator=g)
+    lam = torch.pow(10.0, 3.0 * U).to(cfg.dtype)
+    Q, _ = torch.linalg.qr(G)
+    A = torch.matmul(Q * lam[:, None, :], Q.conj().transpose(-1, -2))
+    return _hermitise(A)
+
+
+def generate(cfg: Config, start: int = 0, count: Optional[int] = None, device="cpu",
+             seed: int = 0) -> torch.Tensor:
+    """Matrices [start, start+count) of config `cfg`'s global batch as a contiguous (AoS)
+    (count, n, n) tensor on `device`."""
+    if count is None:
+        count = cfg.batch - start
+    out = torch.empty(count, cfg.n, cfg.n, dtype=cfg.dtype, device=device)
+    pos = start
+    while pos < start + count:
+        c = pos // CHUNK
+        c0 = c * CHUNK
+        take = min(c0 + CHUNK, start + count) - pos
+        chunk = _gen_chunk(cfg, c, CHUNK, device, seed)
+        out[pos - start:pos - start + take] = chunk[pos - c0:pos - c0 + take]
+        pos += take
+    return out
+
+
+def soa_view(planes: torch.Tensor, batch: int, n: int) -> torch.Tensor:
+    """(batch, n, n) view of an interleaved buffer `planes` of shape (n*n, ld), ld >= batch:
+    element (i, j) of matrix b at planes[i*n + j, b]."""
+    ld = planes.shape[1]
+    return torch.as_strided(planes, (batch, n, n), (1, n * ld, ld))
+
+
+def to_layout(A: torch.Tensor, layout: str, ld: Optional[int] = None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Copy contiguous (batch, n, n) matrices into `layout`.  Returns (storage, view)."""
+    batch, n = A.shape[0], A.shape[1]
+    if layout == "aos":
+        buf = A.contiguous()
+        return buf, buf
+    ld = batch if ld is None else ld
+    planes = torch.empty(n * n, ld, dtype=A.dtype, device=A.device)
+    planes[:, :batch] = A.reshape(batch, n * n).t()
+    if ld > batch:
+        planes[:, batch:] = float("nan")
+    return planes, soa_view(planes, batch, n)
+
+
+def empty_like_layout(view: torch.Tensor) -> torch.Tensor:
+    """Output tensor with the same (batch, n, n) strides as `view`."""
+    return torch.empty_strided(view.shape, view.stride(), dtype=view.dtype, device=view.device)
+
+
+def shard(rank: int, world: int, batch: int) -> Tuple[int, int]:
+    """Contiguous slice [start, start+count) of `batch` owned by `rank` of `world`."""
+    base, rem = divmod(batch, world)
+    start = rank * base + min(rank, rem)
+    return start, base + (1 if rank < rem else 0)
