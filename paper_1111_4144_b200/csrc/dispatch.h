@@ -1,0 +1,35 @@
+// dispatch.h -- internal (not part of the C ABI): per-family launchers, one translation unit
+// per kernel family so the sm_100a instantiations compile in parallel.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hpdinv {
+
+struct LaunchArgs {
+    int64_t batch;
+    int n;
+    const void* A;
+    int64_t sAm, sAe;
+    void* X;
+    int64_t sXm, sXe;
+    int32_t* info;
+    cudaStream_t stream;
+};
+
+constexpr int kNoKernel = -1000;   // launcher has no instantiation for this n
+
+// Each returns 0 / cudaError_t of the launch, or kNoKernel.
+int launch_reg(int dtype, bool ldl, const LaunchArgs& a);       // k_reg.cu
+int launch_lane(int dtype, bool ldl, const LaunchArgs& a);      // k_lane_c64.cu / k_lane_c128.cu
+int launch_generic(int dtype, bool ldl, const LaunchArgs& a);   // k_generic.cu
+
+// Largest n of each family per dtype (0 = c64, 1 = c128).
+constexpr int reg_max_n(int dtype) { return dtype == 0 ? 8 : 6; }
+constexpr int lane_max_n(int dtype) { return dtype == 0 ? 24 : 16; }
+
+// Raise the dynamic shared-memory limit of `fn` on the current device once (thread-safe).
+cudaError_t ensure_smem(const void* fn, size_t bytes);
+
+}  // namespace hpdinv

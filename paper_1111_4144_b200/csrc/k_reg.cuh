@@ -29,10 +29,12 @@ k_reg(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
 #pragma unroll
     for (int i = 0; i < N; i++)
 #pragma unroll
-        for (int j = i; j < N; j++) {
-            cplx<T> v = __ldg(Ab + int64_t(i * N + j) * sAe);
-            if (i == j) v.y = T(0);
-            r[upk(N, i, j)] = v;
+        for (int j = 0; j < N; j++) {
+            if (j >= i) {
+                cplx<T> v = __ldg(Ab + int64_t(i * N + j) * sAe);
+                if (i == j) v.y = T(0);
+                r[upk(N, i, j)] = v;
+            }
         }
 
     // ---- S2: factorisation (right-to-left sums in k ascending, as written in eqs. 3-4)
@@ -42,7 +44,8 @@ k_reg(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
         cplx<T> w[N > 1 ? N - 1 : 1];
         T t = r[upk(N, i, i)].x;
 #pragma unroll
-        for (int k = 0; k < i; k++) {
+        for (int k = 0; k < N; k++) {
+            if (k >= i) continue;
             const cplx<T> rki = r[upk(N, k, i)];
             if (LDL) {
                 const T dk = r[upk(N, k, k)].x;             // d_k stored on the diagonal
@@ -67,10 +70,12 @@ k_reg(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
         }
         inv[i] = iv;
 #pragma unroll
-        for (int j = i + 1; j < N; j++) {
+        for (int j = 0; j < N; j++) {
+            if (j <= i) continue;
             cplx<T> s = r[upk(N, i, j)];
 #pragma unroll
-            for (int k = 0; k < i; k++) cfms_conj(s, w[k], r[upk(N, k, j)]);
+            for (int k = 0; k < N; k++)
+                if (k < i) cfms_conj(s, w[k], r[upk(N, k, j)]);
             r[upk(N, i, j)] = cscale(s, iv);
         }
     }
@@ -80,10 +85,12 @@ k_reg(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
     for (int k = N - 1; k >= 0; k--) {
         cplx<T> t[N];
 #pragma unroll
-        for (int j = k + 1; j < N; j++) {
+        for (int j = 0; j < N; j++) {
+            if (j <= k) continue;
             cplx<T> s = czero<T>();
 #pragma unroll
-            for (int m = k + 1; m < N; m++) {
+            for (int m = 0; m < N; m++) {
+                if (m <= k) continue;
                 const cplx<T> xmj = (m <= j) ? r[upk(N, m, j)] : conjz(r[upk(N, j, m)]);
                 cfma(s, r[upk(N, k, m)], xmj);
             }
@@ -91,11 +98,13 @@ k_reg(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
         }
         T s = T(0);
 #pragma unroll
-        for (int m = k + 1; m < N; m++) s = re_dot_conj(s, r[upk(N, k, m)], t[m]);
+        for (int m = 0; m < N; m++)
+            if (m > k) s = re_dot_conj(s, r[upk(N, k, m)], t[m]);
         const T xkk = LDL ? inv[k] - s : inv[k] * (inv[k] - s);
         r[upk(N, k, k)] = mk<T>(xkk, T(0));
 #pragma unroll
-        for (int j = k + 1; j < N; j++) r[upk(N, k, j)] = t[j];
+        for (int j = 0; j < N; j++)
+            if (j > k) r[upk(N, k, j)] = t[j];
     }
 
     // ---- S5: mirror + store
