@@ -4,7 +4,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhpdinv.so")
+LIB_PATH = os.environ.get("HPDINV_LIB") or os.path.join(HERE, "libhpdinv.so")   # override: A/B builds
 
 _lib = None
 

@@ -2,7 +2,7 @@
 // kernel-family selection per (method, dtype, n).  Host code only; the kernel families live
 // in their own translation units (k_reg.cu, k_lane_c64.cu, k_lane_c128.cu, k_generic.cu).
 #include <mutex>
-#include <set>
+#include <map>
 #include <utility>
 
 #include "../../include/hpdinv.h"
@@ -20,14 +20,15 @@ int launch_lane(int dtype, bool ldl, const LaunchArgs& a) {
 cudaError_t ensure_smem(const void* fn, size_t bytes) {
     if (bytes <= 48 * 1024) return cudaSuccess;
     static std::mutex mu;
-    static std::set<std::pair<const void*, int>> done;
+    static std::map<std::pair<const void*, int>, size_t> done;   // (kernel, device) -> bytes set
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lock(mu);
-    if (done.count({fn, dev})) return cudaSuccess;
+    auto it = done.find({fn, dev});
+    if (it != done.end() && it->second >= bytes) return cudaSuccess;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-    if (e == cudaSuccess) done.insert({fn, dev});
+    if (e == cudaSuccess) done[{fn, dev}] = bytes;
     return e;
 }
 
@@ -47,18 +48,20 @@ LayoutClass classify(int64_t batch, int n, int64_t sm, int64_t se) {
     return kInvalid;
 }
 
-enum Family { kReg, kLane, kGeneric };
+enum Family { kReg, kLane, kCta, kGeneric };
 
 Family family(int dtype, int n) {
     if (n <= reg_max_n(dtype)) return kReg;
     if (n <= lane_max_n(dtype)) return kLane;
+    if (n == 64) return kCta;
     return kGeneric;
 }
 
 const char* family_name(Family f, int dtype, bool ldl) {
-    static const char* names[3][2][2] = {
+    static const char* names[4][2][2] = {
         {{"k_reg<c64,chol>", "k_reg<c64,ldl>"}, {"k_reg<c128,chol>", "k_reg<c128,ldl>"}},
         {{"k_lane<c64,chol>", "k_lane<c64,ldl>"}, {"k_lane<c128,chol>", "k_lane<c128,ldl>"}},
+        {{"k_cta64<c64,chol>", "k_cta64<c64,ldl>"}, {"k_cta64<c128,chol>", "k_cta64<c128,ldl>"}},
         {{"k_generic<c64,chol>", "k_generic<c64,ldl>"}, {"k_generic<c128,chol>", "k_generic<c128,ldl>"}},
     };
     return names[f][dtype][ldl ? 1 : 0];
@@ -86,6 +89,7 @@ int run(int dtype, bool ldl, const LaunchArgs& c) {
     switch (family(dtype, c.n)) {
         case kReg: rc = launch_reg(dtype, ldl, c); break;
         case kLane: rc = launch_lane(dtype, ldl, c); break;
+        case kCta: rc = launch_cta(dtype, ldl, c); break;
         case kGeneric: break;
     }
     if (rc == kNoKernel) rc = launch_generic(dtype, ldl, c);

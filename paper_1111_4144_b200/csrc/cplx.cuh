@@ -19,8 +19,17 @@ template <> __device__ __forceinline__ float qnan<float>() { return __int_as_flo
 template <> __device__ __forceinline__ double qnan<double>() { return __longlong_as_double(0x7ff8000000000000ULL); }
 
 // Overloads (not templates: cplx<T> is a non-deduced context).
-#define HPDINV_CPLX_OPS(V, T)                                                                      \
+#define HPDINV_CPLX_COMMON(V, T)                                                                   \
     __device__ __forceinline__ V conjz(V a) { V z; z.x = a.x; z.y = -a.y; return z; }              \
+    /* acc += a * conj(b) */                                                                       \
+    __device__ __forceinline__ void cfma_conjb(V& acc, V a, V b) {                                 \
+        acc.x = fma(a.x, b.x, acc.x); acc.x = fma(a.y, b.y, acc.x);                                \
+        acc.y = fma(a.y, b.x, acc.y); acc.y = fma(-a.x, b.y, acc.y); }                             \
+    /* t + Re(a * conj(b)) */                                                                      \
+    __device__ __forceinline__ T re_dot_conj(T t, V a, V b) { t = fma(a.x, b.x, t); return fma(a.y, b.y, t); } \
+    __device__ __forceinline__ V cscale(V a, T s) { V z; z.x = a.x * s; z.y = a.y * s; return z; }
+
+#define HPDINV_CPLX_SCALAR_MAC(V)                                                                  \
     /* acc += a * b */                                                                             \
     __device__ __forceinline__ void cfma(V& acc, V a, V b) {                                       \
         acc.x = fma(a.x, b.x, acc.x); acc.x = fma(-a.y, b.y, acc.x);                               \
@@ -32,18 +41,60 @@ template <> __device__ __forceinline__ double qnan<double>() { return __longlong
     /* acc -= conj(a) * b */                                                                       \
     __device__ __forceinline__ void cfms_conj(V& acc, V a, V b) {                                  \
         acc.x = fma(-a.x, b.x, acc.x); acc.x = fma(-a.y, b.y, acc.x);                              \
-        acc.y = fma(-a.x, b.y, acc.y); acc.y = fma(a.y, b.x, acc.y); }                             \
-    /* acc += a * conj(b) */                                                                       \
-    __device__ __forceinline__ void cfma_conjb(V& acc, V a, V b) {                                 \
-        acc.x = fma(a.x, b.x, acc.x); acc.x = fma(a.y, b.y, acc.x);                                \
-        acc.y = fma(a.y, b.x, acc.y); acc.y = fma(-a.x, b.y, acc.y); }                             \
-    /* t + Re(a * conj(b)) */                                                                      \
-    __device__ __forceinline__ T re_dot_conj(T t, V a, V b) { t = fma(a.x, b.x, t); return fma(a.y, b.y, t); } \
-    __device__ __forceinline__ V cscale(V a, T s) { V z; z.x = a.x * s; z.y = a.y * s; return z; }
+        acc.y = fma(-a.x, b.y, acc.y); acc.y = fma(a.y, b.x, acc.y); }
 
-HPDINV_CPLX_OPS(float2, float)
-HPDINV_CPLX_OPS(double2, double)
-#undef HPDINV_CPLX_OPS
+HPDINV_CPLX_COMMON(double2, double)
+HPDINV_CPLX_SCALAR_MAC(double2)
+HPDINV_CPLX_COMMON(float2, float)
+
+#ifdef HPDINV_NO_FFMA2
+HPDINV_CPLX_SCALAR_MAC(float2)
+#else
+// fp32 complex multiply-accumulate on the packed FFMA2 path of sm_100a: one complex MAC is two
+// fma.rn.f32x2 with the per-element operand b broadcast as a scalar ((b.re, b.re), (b.im, b.im))
+// and the operand a (the one the kernels share across a lane's columns: an R element read by
+// broadcast) arranged as a pair.  ptxas folds the scalar broadcasts, the swap and the negation
+// into FFMA2 operand modifiers (.F32, .LO_HI, -), so a MAC issues two instructions (plus one
+// FADD per shared a for the conjugated forms).  Every lane is one IEEE fma:
+//   cfma:      re' = fma(b.im, -a.im, fma(b.re, a.re, re)),  im' = fma(b.im, a.re, fma(b.re, a.im, im))
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(unsigned long long v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+// acc += a * b
+__device__ __forceinline__ void cfma(float2& acc, float2 a, float2 b) {
+    unsigned long long c = pk2(acc.x, acc.y);
+    c = ffma2(pk2(b.x, b.x), pk2(a.x, a.y), c);
+    c = ffma2(pk2(b.y, b.y), pk2(-a.y, a.x), c);
+    upk2(c, acc.x, acc.y);
+}
+// acc -= a * b
+__device__ __forceinline__ void cfms(float2& acc, float2 a, float2 b) {
+    unsigned long long c = pk2(acc.x, acc.y);
+    c = ffma2(pk2(b.x, b.x), pk2(-a.x, -a.y), c);
+    c = ffma2(pk2(b.y, b.y), pk2(a.y, -a.x), c);
+    upk2(c, acc.x, acc.y);
+}
+// acc -= conj(a) * b
+__device__ __forceinline__ void cfms_conj(float2& acc, float2 a, float2 b) {
+    unsigned long long c = pk2(acc.x, acc.y);
+    c = ffma2(pk2(b.x, b.x), pk2(-a.x, a.y), c);
+    c = ffma2(pk2(b.y, b.y), pk2(-a.y, -a.x), c);
+    upk2(c, acc.x, acc.y);
+}
+#endif
+#undef HPDINV_CPLX_COMMON
+#undef HPDINV_CPLX_SCALAR_MAC
 
 // IEEE round-to-nearest reciprocal and square root (exact at 1.0; R9).
 __device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }

@@ -34,7 +34,7 @@ struct LaneShape {
     static constexpr int ESZ = int(sizeof(cplx<T>));
     // per-matrix stride (elements): R rows + a row buffer, padded so that the stride in bytes
     // is 16 mod 128: the MPW groups of a warp then read distinct 16-byte bank quads.
-    static constexpr int raw_bytes = (RSZ + N) * ESZ;
+    static constexpr int raw_bytes = (RSZ + N + G) * ESZ;   // row buffer has G spare slots
     static constexpr int MSTR = (((raw_bytes + 127) / 128) * 128 + 16) / ESZ;
     static constexpr size_t smem_bytes = size_t(MPC) * MSTR * ESZ;
 };
@@ -99,28 +99,31 @@ k_lane(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
 #pragma unroll
     for (int i = 0; i < N; i++) {
         const int qi = i % G, si = i / G;
-        const T t = a[si][i].x;                         // meaningful on the owner lane
-        T piv, iv;
-        if (LDL) { piv = t; iv = rcp_rn(t); }
-        else { piv = sqrt_rn(t); iv = rcp_rn(piv); }
-        (void)piv;
+        // only the owner lane's value is meaningful; the others feed 1.0 so that no lane takes
+        // the (called) slow path of the IEEE sqrt / reciprocal on a garbage operand
+        const T t = (q == qi) ? a[si][i].x : T(1);
+        T iv;
+        if (LDL) iv = rcp_rn(t);
+        else iv = rcp_rn(sqrt_rn(t));
         int bad = !(t > T(0));
         iv = __shfl_sync(FULL, iv, qi, G);
         bad = __shfl_sync(FULL, bad, qi, G);
         if (bad && inf == 0) inf = i + 1;
         inv[i] = iv;
+        // Branch-free SIMT: every statically possible (slot, row) update is executed by all
+        // lanes; for a lane whose column j is not active the update lands on storage that is
+        // dead for that column (strict lower part of A, rows <= j of a finished pivot), so only
+        // the shared-memory stores need a predicate.
         cplx<T> u[C];
         cplx<T>* Ri = Rs + S::roff(i);
 #pragma unroll
         for (int s = 0; s < C; s++) {
             const int j = q + G * s;
             if (G * s + G - 1 > i) {
-                if (j > i && j < N) {
-                    u[s] = a[s][i];
-                    const cplx<T> r = cscale(u[s], iv);
-                    a[s][i] = r;
-                    Ri[j - i] = r;
-                }
+                u[s] = a[s][i];
+                const cplx<T> r = cscale(u[s], iv);
+                a[s][i] = r;
+                if (j > i) Ri[j - i] = r;
             }
         }
         __syncwarp();
@@ -135,10 +138,7 @@ k_lane(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
                 if (l > i && l < N) {
 #pragma unroll
                     for (int s = 0; s < C; s++) {
-                        const int j = q + G * s;
-                        if (G * s + G - 1 >= l) {
-                            if (j >= l && j < N) cfms_conj(a[s][l], e[h], LDL ? u[s] : a[s][i]);
-                        }
+                        if (G * s + G - 1 >= l) cfms_conj(a[s][l], e[h], LDL ? u[s] : a[s][i]);
                     }
                 }
             }
@@ -147,6 +147,10 @@ k_lane(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
 
     // ------------------------------------------------ S3/S4: proposed inversion, rows k = n..1
     cplx<T> x[C][N];
+#pragma unroll
+    for (int s = 0; s < C; s++)
+#pragma unroll
+        for (int m = 0; m < N; m++) x[s][m] = czero<T>();
 #pragma unroll
     for (int k = N - 1; k >= 0; k--) {
         const int qk = k % G, sk = k / G;
@@ -165,11 +169,12 @@ k_lane(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
                 if (l > k && l < N) {
 #pragma unroll
                     for (int s = 0; s < C; s++) {
-                        const int j = q + G * s;
                         if (G * s + G - 1 > k) {
-                            if (j > k && j < N) cfma(acc[s], e[h], x[s][l]);
+                            cfma(acc[s], e[h], x[s][l]);
                             if (l >= G * s && l <= G * s + G - 1) {
-                                if (j == l) rkj[s] = e[h];
+                                const bool hit = (q + G * s) == l;
+                                rkj[s].x = hit ? e[h].x : rkj[s].x;
+                                rkj[s].y = hit ? e[h].y : rkj[s].y;
                             }
                         }
                     }
@@ -181,32 +186,36 @@ k_lane(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
         for (int s = 0; s < C; s++) {
             const int j = q + G * s;
             if (G * s + G - 1 > k) {
-                if (j > k && j < N) {
-                    const cplx<T> xv = LDL ? mk<T>(-acc[s].x, -acc[s].y) : cscale(acc[s], -inv[k]);
-                    x[s][k] = xv;
-                    rowbuf[j] = xv;
-                    p = re_dot_conj(p, rkj[s], xv);
-                }
+                // for j <= k the value is dead: x[s][k] of such a column is rewritten by the
+                // gather (j < k) or by the diagonal (j == k) before it is read
+                const cplx<T> xv = LDL ? mk<T>(-acc[s].x, -acc[s].y) : cscale(acc[s], -inv[k]);
+                x[s][k] = xv;
+                rowbuf[j] = xv;
+                p = re_dot_conj(p, rkj[s], xv);         // rkj[s] == 0 unless j > k
             }
         }
 #pragma unroll
         for (int off = 1; off < G; off <<= 1) p += __shfl_xor_sync(FULL, p, off, G);
         __syncwarp();
-        if (q == qk) {
+        const bool own = (q == qk);                     // this lane owns column k
 #pragma unroll
-            for (int o = 0; o < N; o += P) {
-                if (o + P - 1 <= k) continue;
-                cplx<T> e[2];
-                lds_pair<T>(rowbuf, o, e[0], e[1]);      // aligned pair holding element o
+        for (int o = 0; o < N; o += P) {
+            if (o + P - 1 <= k) continue;
+            cplx<T> e[2];
+            lds_pair<T>(rowbuf, o, e[0], e[1]);          // aligned pair holding element o
 #pragma unroll
-                for (int h = 0; h < P; h++) {
-                    const int m = o + h;
-                    if (m > k && m < N) x[sk][m] = conjz(e[h]);
+            for (int h = 0; h < P; h++) {
+                const int m = o + h;
+                if (m > k && m < N) {
+                    x[sk][m].x = own ? e[h].x : x[sk][m].x;
+                    x[sk][m].y = own ? -e[h].y : x[sk][m].y;
                 }
             }
-            const T ik = inv[k];
-            x[sk][k] = mk<T>(LDL ? ik - p : ik * (ik - p), T(0));
         }
+        const T ik = inv[k];
+        const T xkk = LDL ? ik - p : ik * (ik - p);
+        x[sk][k].x = own ? xkk : x[sk][k].x;
+        x[sk][k].y = own ? T(0) : x[sk][k].y;
         __syncwarp();
     }
 

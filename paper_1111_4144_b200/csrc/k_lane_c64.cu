@@ -2,6 +2,10 @@
 #include "dispatch.h"
 #include "k_lane.cuh"
 
+#ifndef HPDINV_G32
+#define HPDINV_G32 16   // lanes per matrix for n = 25..32
+#endif
+
 namespace hpdinv {
 
 template <bool LDL>
@@ -22,6 +26,8 @@ static int launch_lane_c64(const LaunchArgs& a) {
         HPDINV_LANE(13, 4) HPDINV_LANE(14, 4) HPDINV_LANE(15, 4) HPDINV_LANE(16, 4)
         HPDINV_LANE(17, 8) HPDINV_LANE(18, 8) HPDINV_LANE(19, 8) HPDINV_LANE(20, 8)
         HPDINV_LANE(21, 8) HPDINV_LANE(22, 8) HPDINV_LANE(23, 8) HPDINV_LANE(24, 8)
+        HPDINV_LANE(25, HPDINV_G32) HPDINV_LANE(26, HPDINV_G32) HPDINV_LANE(27, HPDINV_G32) HPDINV_LANE(28, HPDINV_G32)
+        HPDINV_LANE(29, HPDINV_G32) HPDINV_LANE(30, HPDINV_G32) HPDINV_LANE(31, HPDINV_G32) HPDINV_LANE(32, HPDINV_G32)
         default: break;
     }
 #undef HPDINV_LANE
