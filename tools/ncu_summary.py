@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Summarise an ncu --set full report (one or more kernels) into a short text table.
 
-    python tools/ncu_summary.py gpurun_out/prof.ncu-rep [out.txt] [--traffic cfgK batch]
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep [out.txt] [--traffic cfgK batch k_family<c64,chol>]
 """
 import csv
 import io
@@ -65,14 +65,14 @@ def main():
         open(out, "w").write("# ncu --set full summary of %s\n%s\n" % (os.path.basename(rep), text))
     if "--traffic" in sys.argv:
         i = sys.argv.index("--traffic")
-        cfg, batch = sys.argv[i + 1], int(sys.argv[i + 2])
+        cfg, batch, short = sys.argv[i + 1], int(sys.argv[i + 2]), sys.argv[i + 3]
         d = load(rep)[0]
         mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         tb = sum(float(d[k][1].replace(",", "")) * mult[d[k][0]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json")
         t = json.load(open(path)) if os.path.exists(path) else {}
         name = d["Kernel Name"][1]
-        t[cfg] = {"kernel_full": name, "batch": batch, "dram_bytes_per_launch": tb, "source": os.path.basename(rep)}
+        t[cfg] = {"kernel_full": name, "kernel": short, "batch": batch, "dram_bytes_per_launch": tb, "source": os.path.basename(rep)}
         json.dump(t, open(path, "w"), indent=1)
         print("traffic", cfg, tb)
 
