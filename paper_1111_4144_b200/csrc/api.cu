@@ -48,21 +48,25 @@ LayoutClass classify(int64_t batch, int n, int64_t sm, int64_t se) {
     return kInvalid;
 }
 
-enum Family { kReg, kLane, kCta, kGeneric };
+enum Family { kReg, kLane, kCta, kGeneric, kGrp };
 
-Family family(int dtype, int n) {
+// interleaved A and X at n = 9..16 (c64): in-place lane groups (k_grp); otherwise the general
+// lane-group kernel (k_lane)
+Family family(int dtype, int n, bool soa) {
     if (n <= reg_max_n(dtype)) return kReg;
+    if (soa && dtype == 0 && n <= grp_max_n(dtype)) return kGrp;
     if (n <= lane_max_n(dtype)) return kLane;
     if (n == 64) return kCta;
     return kGeneric;
 }
 
 const char* family_name(Family f, int dtype, bool ldl) {
-    static const char* names[4][2][2] = {
+    static const char* names[5][2][2] = {
         {{"k_reg<c64,chol>", "k_reg<c64,ldl>"}, {"k_reg<c128,chol>", "k_reg<c128,ldl>"}},
         {{"k_lane<c64,chol>", "k_lane<c64,ldl>"}, {"k_lane<c128,chol>", "k_lane<c128,ldl>"}},
         {{"k_cta64<c64,chol>", "k_cta64<c64,ldl>"}, {"k_cta64<c128,chol>", "k_cta64<c128,ldl>"}},
         {{"k_generic<c64,chol>", "k_generic<c64,ldl>"}, {"k_generic<c128,chol>", "k_generic<c128,ldl>"}},
+        {{"k_grp<c64,chol>", "k_grp<c64,ldl>"}, {"k_grp<c128,chol>", "k_grp<c128,ldl>"}},
     };
     return names[f][dtype][ldl ? 1 : 0];
 }
@@ -86,12 +90,15 @@ int run(int dtype, bool ldl, const LaunchArgs& c) {
     const int v = validate(c, dtype == 0 ? 8 : 16);
     if (v <= 0) return v;
     int rc = kNoKernel;
-    switch (family(dtype, c.n)) {
+    const bool soa = classify(c.batch, c.n, c.sAm, c.sAe) == kSoA && classify(c.batch, c.n, c.sXm, c.sXe) == kSoA;
+    switch (family(dtype, c.n, soa)) {
         case kReg: rc = launch_reg(dtype, ldl, c); break;
+        case kGrp: rc = launch_grp(dtype, ldl, c); break;
         case kLane: rc = launch_lane(dtype, ldl, c); break;
         case kCta: rc = launch_cta(dtype, ldl, c); break;
         case kGeneric: break;
     }
+    if (rc == kNoKernel && c.n <= lane_max_n(dtype)) rc = launch_lane(dtype, ldl, c);   // k_grp declined
     if (rc == kNoKernel) rc = launch_generic(dtype, ldl, c);
     return rc;
 }
@@ -129,7 +136,8 @@ const char* hpdinv_kernel_name(int method, int dtype, int64_t batch, int n, int6
     if (batch < 0 || n < 1 || n > HPDINV_MAX_N || dtype < 0 || dtype > 1) return nullptr;
     if (classify(batch, n, sAm, sAe) == kInvalid || classify(batch, n, sXm, sXe) == kInvalid)
         return nullptr;
-    return family_name(family(dtype, n), dtype, method != 0);
+    const bool soa = classify(batch, n, sAm, sAe) == kSoA && classify(batch, n, sXm, sXe) == kSoA;
+    return family_name(family(dtype, n, soa), dtype, method != 0);
 }
 
 const char* hpdinv_version(void) { return "hpdinv 0.2.0 (sm_100a)"; }

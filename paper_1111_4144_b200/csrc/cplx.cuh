@@ -93,6 +93,112 @@ __device__ __forceinline__ void cfms_conj(float2& acc, float2 a, float2 b) {
     upk2(c, acc.x, acc.y);
 }
 #endif
+
+// acc += a * conj(b)   (fp32: two FFMA2, scalar operand b broadcast; fp64: four DFMA)
+__device__ __forceinline__ void cfma_cb(double2& acc, double2 a, double2 b) {
+    acc.x = fma(a.x, b.x, acc.x); acc.x = fma(a.y, b.y, acc.x);
+    acc.y = fma(a.y, b.x, acc.y); acc.y = fma(-a.x, b.y, acc.y);
+}
+#ifdef HPDINV_NO_FFMA2
+__device__ __forceinline__ void cfma_cb(float2& acc, float2 a, float2 b) {
+    acc.x = fmaf(a.x, b.x, acc.x); acc.x = fmaf(a.y, b.y, acc.x);
+    acc.y = fmaf(a.y, b.x, acc.y); acc.y = fmaf(-a.x, b.y, acc.y);
+}
+#else
+__device__ __forceinline__ void cfma_cb(float2& acc, float2 a, float2 b) {
+    unsigned long long c = pk2(acc.x, acc.y);
+    c = ffma2(pk2(b.x, b.x), pk2(a.x, a.y), c);
+    c = ffma2(pk2(b.y, b.y), pk2(a.y, -a.x), c);
+    upk2(c, acc.x, acc.y);
+}
+#endif
+
+// "Shared-multiplier" complex MAC.  The kernels' inner loops multiply one operand a, reused
+// across a whole row of MACs, by a stream of per-use operands x.  PMul<T> holds a in the form
+// the MAC wants; PAcc<T> is the accumulator.  fp32 (FFMA2 path): a*x = x.re*(a.re, a.im) +
+// x.im*(-a.im, a.re), so with p = (a.re, a.im) and q = (-a.im, a.re) precomputed once, one MAC
+// is two fma.rn.f32x2 whose scalar operand (x.re or x.im) is broadcast to both lanes; the
+// accumulator stays packed in one 64-bit register pair.  fp64: plain DFMA.
+template <typename T> struct PMul;
+template <typename T> struct PAcc;
+template <> struct PMul<double> { double2 a; };
+template <> struct PAcc<double> { double2 v; };
+__device__ __forceinline__ PMul<double> pmul(double2 a) { return PMul<double>{a}; }
+__device__ __forceinline__ PAcc<double> pacc(double2 v) { return PAcc<double>{v}; }
+__device__ __forceinline__ double2 pval(PAcc<double> c) { return c.v; }
+__device__ __forceinline__ void pmac(PAcc<double>& c, const PMul<double>& m, double2 x) { cfma(c.v, m.a, x); }
+__device__ __forceinline__ void pmac_cb(PAcc<double>& c, const PMul<double>& m, double2 x) { cfma_cb(c.v, m.a, x); }
+#ifdef HPDINV_NO_FFMA2
+template <> struct PMul<float> { float2 a; };
+template <> struct PAcc<float> { float2 v; };
+__device__ __forceinline__ PMul<float> pmul(float2 a) { return PMul<float>{a}; }
+__device__ __forceinline__ PAcc<float> pacc(float2 v) { return PAcc<float>{v}; }
+__device__ __forceinline__ float2 pval(PAcc<float> c) { return c.v; }
+__device__ __forceinline__ void pmac(PAcc<float>& c, const PMul<float>& m, float2 x) { cfma(c.v, m.a, x); }
+__device__ __forceinline__ void pmac_cb(PAcc<float>& c, const PMul<float>& m, float2 x) { cfma_cb(c.v, m.a, x); }
+#else
+template <> struct PMul<float> { unsigned long long p, q; };
+template <> struct PAcc<float> { unsigned long long v; };
+__device__ __forceinline__ PMul<float> pmul(float2 a) { return PMul<float>{pk2(a.x, a.y), pk2(-a.y, a.x)}; }
+__device__ __forceinline__ PAcc<float> pacc(float2 v) { return PAcc<float>{pk2(v.x, v.y)}; }
+__device__ __forceinline__ float2 pval(PAcc<float> c) { float2 z; upk2(c.v, z.x, z.y); return z; }
+// c += a * x
+__device__ __forceinline__ void pmac(PAcc<float>& c, const PMul<float>& m, float2 x) {
+    c.v = ffma2(pk2(x.x, x.x), m.p, c.v);
+    c.v = ffma2(pk2(x.y, x.y), m.q, c.v);
+}
+// c += a * conj(x)
+__device__ __forceinline__ void pmac_cb(PAcc<float>& c, const PMul<float>& m, float2 x) {
+    c.v = ffma2(pk2(x.x, x.x), m.p, c.v);
+    c.v = ffma2(pk2(-x.y, -x.y), m.q, c.v);
+}
+#endif
+
+// Split accumulator for a MAC whose shared operand is the STREAMED one: acc += r * x with r the
+// pair (r.re, r.im) as loaded and x broadcast per component.  fp32: the two partial sums
+// a = sum x.re * r and b = sum x.im * r are two FFMA2 with no operand rearrangement at all;
+// the value is a + i*b = (a.re - b.im, a.im + b.re), formed once at the end.  fp64: one cfma.
+template <typename T> struct SAcc;
+template <> struct SAcc<double> { double2 v; };
+__device__ __forceinline__ void sacc_zero(SAcc<double>& c) { c.v = make_double2(0.0, 0.0); }
+__device__ __forceinline__ void smac(SAcc<double>& c, double2 r, double2 x) { cfma(c.v, r, x); }
+__device__ __forceinline__ double2 sval(const SAcc<double>& c) { return c.v; }
+#ifdef HPDINV_NO_FFMA2
+template <> struct SAcc<float> { float2 v; };
+__device__ __forceinline__ void sacc_zero(SAcc<float>& c) { c.v = make_float2(0.f, 0.f); }
+__device__ __forceinline__ void smac(SAcc<float>& c, float2 r, float2 x) { cfma(c.v, r, x); }
+__device__ __forceinline__ float2 sval(const SAcc<float>& c) { return c.v; }
+#else
+template <> struct SAcc<float> { unsigned long long a, b; };
+__device__ __forceinline__ void sacc_zero(SAcc<float>& c) { c.a = 0ull; c.b = 0ull; }
+__device__ __forceinline__ void smac(SAcc<float>& c, float2 r, float2 x) {
+    const unsigned long long rp = pk2(r.x, r.y);
+    c.a = ffma2(pk2(x.x, x.x), rp, c.a);
+    c.b = ffma2(pk2(x.y, x.y), rp, c.b);
+}
+__device__ __forceinline__ float2 sval(const SAcc<float>& c) {
+    float ax, ay, bx, by;
+    upk2(c.a, ax, ay);
+    upk2(c.b, bx, by);
+    return make_float2(ax - by, ay + bx);
+}
+#endif
+
+// elementwise (a.re*b.re + c.re, a.im*b.im + c.im): one FFMA2 for fp32 (Re(a conj(b)) partial sums)
+__device__ __forceinline__ double2 pfma_elem(double2 a, double2 b, double2 c) {
+    return make_double2(fma(a.x, b.x, c.x), fma(a.y, b.y, c.y));
+}
+#ifdef HPDINV_NO_FFMA2
+__device__ __forceinline__ float2 pfma_elem(float2 a, float2 b, float2 c) {
+    return make_float2(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y));
+}
+#else
+__device__ __forceinline__ float2 pfma_elem(float2 a, float2 b, float2 c) {
+    float2 z;
+    upk2(ffma2(pk2(a.x, a.y), pk2(b.x, b.y), pk2(c.x, c.y)), z.x, z.y);
+    return z;
+}
+#endif
 #undef HPDINV_CPLX_COMMON
 #undef HPDINV_CPLX_SCALAR_MAC
 
@@ -101,6 +207,22 @@ __device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
 __device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
 __device__ __forceinline__ float sqrt_rn(float x) { return __fsqrt_rn(x); }
 __device__ __forceinline__ double sqrt_rn(double x) { return __dsqrt_rn(x); }
+
+// Short-latency pivot reciprocals for the fp32 lane-group kernels: hardware approximation
+// (MUFU, ~2^-22 relative) plus one Newton step, exact when the operand is 1.0 (so the exact
+// integer families stay bit-exact; R9).  1/sqrt(t) for Cholesky, 1/t for LDL.
+__device__ __forceinline__ float rsqrt_nr(float t) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(t));
+    const float e = fmaf(-t * y, y, 1.0f);       // 1 - t y^2
+    return fmaf(0.5f * y, e, y);
+}
+__device__ __forceinline__ float rcp_nr(float t) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(t));
+    const float e = fmaf(-t, y, 1.0f);
+    return fmaf(y, e, y);
+}
 
 // Packed upper-triangle index, row-major: (i, j), i <= j, of an n x n matrix.
 __host__ __device__ constexpr int upk(int n, int i, int j) { return i * n - (i * (i - 1)) / 2 + (j - i); }

@@ -25,10 +25,12 @@ int launch_reg(int dtype, bool ldl, const LaunchArgs& a);       // k_reg.cu
 int launch_lane(int dtype, bool ldl, const LaunchArgs& a);      // k_lane_c64.cu / k_lane_c128.cu
 int launch_generic(int dtype, bool ldl, const LaunchArgs& a);   // k_generic.cu
 int launch_cta(int dtype, bool ldl, const LaunchArgs& a);       // k_cta64.cu (n = 64)
+int launch_grp(int dtype, bool ldl, const LaunchArgs& a);       // k_grp.cu (interleaved, c64 9..16)
 
 // Largest n of each family per dtype (0 = c64, 1 = c128).
 constexpr int reg_max_n(int dtype) { return dtype == 0 ? 8 : 6; }
 constexpr int lane_max_n(int dtype) { return dtype == 0 ? 32 : 16; }
+constexpr int grp_max_n(int dtype) { return dtype == 0 ? 16 : 0; }
 
 // Raise the dynamic shared-memory limit of `fn` on the current device once (thread-safe).
 cudaError_t ensure_smem(const void* fn, size_t bytes);

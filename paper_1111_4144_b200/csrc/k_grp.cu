@@ -1,0 +1,47 @@
+// k_grp.cu -- instantiations and launcher of the in-place lane-group kernel (k_grp.cuh),
+// selected for interleaved (SoA) inputs at n = 9..16 (complex64).
+#include "dispatch.h"
+#include "k_grp.cuh"
+
+namespace hpdinv {
+
+template <typename T, bool LDL>
+static int launch_grp_t(const LaunchArgs& a) {
+    using fn_t = void (*)(int64_t, const cplx<T>*, int64_t, int64_t, cplx<T>*, int64_t, int64_t, int32_t*);
+    fn_t fn = nullptr;
+    size_t smem = 0;
+    int mpc = 1, threads = 0;
+#define HPDINV_GRP(NN)                          \
+    case NN:                                    \
+        fn = k_grp<T, NN, LDL>;                 \
+        smem = GrpShape<T, NN>::smem_bytes;     \
+        mpc = GrpShape<T, NN>::MPC;             \
+        threads = GrpShape<T, NN>::THREADS;     \
+        break;
+    if constexpr (sizeof(T) == 4) {
+        switch (a.n) {
+            HPDINV_GRP(9) HPDINV_GRP(10) HPDINV_GRP(11) HPDINV_GRP(12)
+            HPDINV_GRP(13) HPDINV_GRP(14) HPDINV_GRP(15) HPDINV_GRP(16)
+            default: break;
+        }
+    }
+#undef HPDINV_GRP
+    // plane strides in bytes must fit the kernel's 32-bit address offsets (any SoA array with
+    // n >= 9 that fits in device memory does)
+    const uint64_t lim = uint64_t(1) << 32;
+    if (uint64_t(a.sAe) * sizeof(cplx<T>) >= lim || uint64_t(a.sXe) * sizeof(cplx<T>) >= lim) fn = nullptr;
+    if (!fn) return kNoKernel;
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
+    if (e != cudaSuccess) return int(e);
+    const int64_t blocks = (a.batch + mpc - 1) / mpc;
+    fn<<<unsigned(blocks), threads, smem, a.stream>>>(a.batch, static_cast<const cplx<T>*>(a.A), a.sAm, a.sAe,
+                                                     static_cast<cplx<T>*>(a.X), a.sXm, a.sXe, a.info);
+    return int(cudaGetLastError());
+}
+
+int launch_grp(int dtype, bool ldl, const LaunchArgs& a) {
+    if (dtype == 0) return ldl ? launch_grp_t<float, true>(a) : launch_grp_t<float, false>(a);
+    return kNoKernel;
+}
+
+}  // namespace hpdinv

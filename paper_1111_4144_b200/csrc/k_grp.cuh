@@ -1,0 +1,257 @@
+// k_grp.cuh -- G = 4 lanes per matrix, 8 matrices per warp, every column held IN PLACE in
+// registers: the config-3 kernel (n = 16, complex64, interleaved, 2^22 matrices).
+//
+// Design (why not one matrix per thread): the fully unrolled per-thread code of an n = 16
+// matrix (~9.5k instructions, 150 KB) thrashes the instruction cache ("no_instruction" was the
+// top stall at 6 warps/SM); splitting a matrix over G lanes divides the straight-line code per
+// thread by G, and holding the columns in registers needs no shared-memory round trip per MAC.
+//
+// Lane q of a group owns the columns j = q + G*s (s = 0..C-1), dealt cyclically so all lanes
+// have nearly the same active work at every step.  col[s][0..n-1] is column j of ONE working
+// matrix that is, at every moment, R above the current row and X below it (App. A.1: row k of
+// R is consumed by row k of X), so each lane holds n*C complex values and nothing else:
+//   S1  load a_lj, l <= j (predicated: the strict lower part is never read);
+//   S2  right-looking Cholesky (eqs. 3-4) / LDL (eqs. 10-11): at step i the owner of column i
+//       forms the pivot t (info = first i with !(t > 0)), 1/r_ii (1/d_i) is broadcast by
+//       shuffle, each lane scales its entries of row i and stores them in the group's packed
+//       row store in shared memory; every lane then reads row i back (16-byte broadcast loads)
+//       and updates a_lj -= conj(r_il) r_ij (LDL: conj(r_il) d_i r_ij), k = i ascending as in
+//       the sums of eqs. 3-4;
+//   S3  S = diag(1/r_ii) (eq. 24) / S~ = diag(1/d_i) (eq. 29): the reciprocals, kept in smem;
+//   S4  rows k = n-1..0 (eqs. 22-24 / 27-29): R row k is read back from the row store; lane j
+//       forms x_kj = -(1/r_kk) sum_{m>k} r_km x~_mj over its register column (x~_mj for m > k
+//       is already X: the upper part computed in rows > k, the lower part gathered below);
+//       the new row goes through a row buffer to the owner of column k, which stores it
+//       conjugated as the lower part of column k (x_mk = conj(x_km), the mirror) and forms
+//       x_kk = (1/r_kk)(1/r_kk - Re sum_{m>k} r_km conj(x_km)) real;
+//   S5  every lane stores its columns (lower part: the bitwise conjugate written in S4).
+// Dead storage is reused freely: a lane whose column j is not active at a step computes on
+// entries of column j that are rewritten before they are read (lower part before its gather,
+// rows <= j of a finished pivot), so the SIMT code needs no per-lane predicate except on the
+// shared-memory stores.
+#pragma once
+#include "cplx.cuh"
+
+namespace hpdinv {
+
+template <typename T, int N>
+struct GrpShape {
+    static constexpr int G = 4;                       // lanes per matrix
+    static constexpr int C = (N + G - 1) / G;         // columns per lane
+    static constexpr int MPW = 32 / G;                // matrices per warp
+    static constexpr int WARPS = 4;
+    static constexpr int THREADS = 32 * WARPS;
+    static constexpr int MPC = MPW * WARPS;           // matrices per CTA
+#ifndef HPDINV_GRP_MINB
+#define HPDINV_GRP_MINB 3
+#endif
+    static constexpr int MIN_BLOCKS = HPDINV_GRP_MINB;  // 3: caps ptxas at 170 registers, 12 warps/SM
+    static constexpr int P = sizeof(T) == 4 ? 2 : 1;  // complex elements per 16-byte load
+    // packed row store: row i holds j = i..n-1 at offset roff(i) + (j - i), 16-byte aligned
+    __host__ __device__ static constexpr int rlen(int i) { return ((N - i) + P - 1) / P * P; }
+    __host__ __device__ static constexpr int roff(int i) { int o = 0; for (int k = 0; k < i; k++) o += rlen(k); return o; }
+    static constexpr int RSZ = roff(N);
+    static constexpr int ESZ = int(sizeof(cplx<T>));
+    // per matrix: row store + X row buffer (n, padded) + reciprocals (n reals); the stride in
+    // bytes is 16 mod 128 so the MPW groups of a warp hit distinct 16-byte bank quads
+    static constexpr int raw_bytes = (RSZ + (N + P - 1) / P * P) * ESZ + ((N * int(sizeof(T)) + 15) / 16) * 16;
+    static constexpr int MSTR_B = ((raw_bytes + 127) / 128) * 128 + 16;
+    static constexpr size_t smem_bytes = size_t(MPC) * MSTR_B;
+};
+
+namespace grp {
+template <typename T>
+__device__ __forceinline__ void lds_pair(const cplx<T>* p, int o, cplx<T>& e0, cplx<T>& e1) {
+    if constexpr (sizeof(T) == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(p + (o & ~1));
+        e0 = make_float2(v.x, v.y);
+        e1 = make_float2(v.z, v.w);
+    } else {
+        e0 = p[o];
+        e1 = e0;
+    }
+}
+}  // namespace grp
+
+template <typename T, int N, bool LDL>
+__global__ void __launch_bounds__(GrpShape<T, N>::THREADS, GrpShape<T, N>::MIN_BLOCKS)
+k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
+      cplx<T>* X, int64_t sXm, int64_t sXe, int32_t* __restrict__ info)
+{
+    using Sh = GrpShape<T, N>;
+    using V = cplx<T>;
+    constexpr int G = Sh::G, C = Sh::C, P = Sh::P;
+    constexpr unsigned FULL = 0xffffffffu;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q = lane & (G - 1), g = lane / G;
+    const int mloc = warp * Sh::MPW + g;
+    int64_t b = int64_t(blockIdx.x) * Sh::MPC + mloc;
+    const bool valid = b < batch;
+    b = valid ? b : batch - 1;                        // the tail recomputes (never stores) the last matrix
+    unsigned char* mbase = smem_raw + size_t(mloc) * Sh::MSTR_B;
+    V* Rs = reinterpret_cast<V*>(mbase);                              // packed R rows
+    V* rowbuf = Rs + Sh::RSZ;                                         // X row k
+    T* invs = reinterpret_cast<T*>(rowbuf + (N + P - 1) / P * P);     // 1/r_kk or 1/d_k
+
+    // ---------------------------------------------------------------- S1: load columns
+    // (entries below the diagonal of a column are dead storage; Im a_jj is never read)
+    V col[C][N];
+    {
+        // element (l, j = q + G*s): lane base + (l*n + G*s) * plane stride; the plane stride in
+        // bytes is < 2^32 (checked by the launcher), so each address is one IMAD.WIDE
+        const char* Ab = reinterpret_cast<const char*>(A + b * sAm + q * sAe);
+        const uint32_t seA = uint32_t(sAe * int64_t(sizeof(V)));
+#pragma unroll
+        for (int s = 0; s < C; s++) {
+            const int j = q + G * s;
+#pragma unroll
+            for (int l = 0; l < N; l++) {
+                col[s][l] = czero<T>();
+                if (l <= G * s + G - 1 && l <= j && j < N)
+                    col[s][l] = __ldg(reinterpret_cast<const V*>(Ab + uint64_t(uint32_t(l * N + G * s)) * seA));
+            }
+        }
+    }
+
+    // -------------------------------------------------------- S2: right-looking factorisation
+    int inf = 0;
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+        const int qi = i % G, si = i / G;
+        const T t = (q == qi) ? col[si][i].x : T(1);    // non-owners feed 1: no slow paths
+        const int bad0 = !(t > T(0));
+        const T tt = bad0 ? T(1) : t;
+        T iv;
+        iv = LDL ? rcp_rn(tt) : rcp_rn(sqrt_rn(tt));
+        iv = __shfl_sync(FULL, iv, qi, G);
+        const int bad = __shfl_sync(FULL, bad0, qi, G);
+        T di = T(0);
+        if (LDL) di = __shfl_sync(FULL, tt, qi, G);
+        if (bad && inf == 0) inf = i + 1;
+        if (q == 0) invs[i] = iv;
+        V* Ri = Rs + Sh::roff(i);
+        PMul<T> mul[C];
+#pragma unroll
+        for (int s = 0; s < C; s++) {
+            if (G * s + G - 1 > i) {
+                const int j = q + G * s;
+                const V u = col[s][i];                   // a'_ij (unscaled)
+                const V r = cscale(u, iv);               // r_ij (eq. 4 / eq. 11)
+                col[s][i] = r;
+                if (j > i && j < N) Ri[j - i] = r;
+                // a'_lj -= conj(r_il) * r_ij (Cholesky) or conj(r_il) * d_i r_ij (LDL)
+                const V w = LDL ? cscale(r, di) : r;
+                mul[s] = pmul(mk<T>(-w.x, -w.y));
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int o0 = 0; o0 < N; o0 += P) {
+            if (o0 >= N - i) continue;
+            V e[2];
+            grp::lds_pair<T>(Ri, o0, e[0], e[1]);        // r_il, l = i + o0 + h
+#pragma unroll
+            for (int h = 0; h < P; h++) {
+                const int oo = o0 + h;
+                if (oo < 1 || oo >= N - i) continue;
+                const int l = i + oo;
+#pragma unroll
+                for (int s = 0; s < C; s++) {
+                    if (G * s + G - 1 >= l && G * s + G - 1 > i) {
+                        PAcc<T> a = pacc(col[s][l]);
+                        pmac_cb(a, mul[s], e[h]);
+                        col[s][l] = pval(a);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+
+    // ------------------------------------------------ S3/S4: proposed inversion, rows k = n..1
+#pragma unroll
+    for (int k = N - 1; k >= 0; k--) {
+        const int qk = k % G, sk = k / G;
+        const V* Rk = Rs + Sh::roff(k);
+        const T ik = invs[k];
+        V rk[N];                                        // r_km, m > k
+#pragma unroll
+        for (int o = 0; o < N; o += P) {
+            if (o >= N - k) continue;
+            V e0, e1;
+            grp::lds_pair<T>(Rk, o, e0, e1);
+            if (o >= 1) rk[k + o] = e0;
+            if (P == 2 && o + 1 < N - k) rk[k + o + 1] = e1;
+        }
+        SAcc<T> acc[C];
+#pragma unroll
+        for (int s = 0; s < C; s++) sacc_zero(acc[s]);
+#pragma unroll
+        for (int m = 0; m < N; m++) {
+            if (m <= k) continue;
+#pragma unroll
+            for (int s = 0; s < C; s++)
+                if (G * s + G - 1 > k) smac(acc[s], rk[m], col[s][m]);
+        }
+        V xk[C];
+#pragma unroll
+        for (int s = 0; s < C; s++) {
+            if (G * s + G - 1 > k) {
+                const V a = sval(acc[s]);
+                xk[s] = LDL ? mk<T>(-a.x, -a.y) : cscale(a, -ik);
+                col[s][k] = xk[s];
+                const int j = q + G * s;
+                if (j > k && j < N) rowbuf[j] = xk[s];
+            }
+        }
+        __syncwarp();
+        if (q == qk) {
+            // the owner of column k takes row k of X as its lower part (mirror) and forms x_kk
+            // p = Re sum_{m>k} r_km conj(x_km), m ascending, as (re*re, im*im) lane pairs
+            V pp = czero<T>();
+#pragma unroll
+            for (int o = 0; o < N; o += P) {
+                if (o + P - 1 <= k) continue;
+                V e[2];
+                grp::lds_pair<T>(rowbuf, o, e[0], e[1]);
+#pragma unroll
+                for (int h = 0; h < P; h++) {
+                    const int m = o + h;
+                    if (m > k && m < N) {
+                        col[sk][m] = conjz(e[h]);
+                        pp = pfma_elem(rk[m], e[h], pp);
+                    }
+                }
+            }
+            const T p = pp.x + pp.y;
+            col[sk][k] = mk<T>(LDL ? ik - p : ik * (ik - p), T(0));
+        }
+        __syncwarp();
+    }
+
+    // ------------------------------------------------------------------ S5: mirror + store
+    if (valid) {
+        V* Xb = X + b * sXm;
+        char* Xq = reinterpret_cast<char*>(Xb + q * sXe);
+        const uint32_t seX = uint32_t(sXe * int64_t(sizeof(V)));
+#pragma unroll
+        for (int s = 0; s < C; s++) {
+            const int j = q + G * s;
+            if (j < N) {
+#pragma unroll
+                for (int m = 0; m < N; m++)
+                    *reinterpret_cast<V*>(Xq + uint64_t(uint32_t(m * N + G * s)) * seX) = col[s][m];
+            }
+        }
+        if (inf) {          // a flagged matrix is overwritten (same thread, program order)
+            const T nan = qnan<T>();
+#pragma unroll 1
+            for (int e = q; e < N * N; e += G) Xb[int64_t(e) * sXe] = mk<T>(nan, nan);
+        }
+        if (q == 0) info[b] = inf;
+    }
+}
+
+}  // namespace hpdinv
