@@ -48,25 +48,27 @@ LayoutClass classify(int64_t batch, int n, int64_t sm, int64_t se) {
     return kInvalid;
 }
 
-enum Family { kReg, kLane, kCta, kGeneric, kGrp };
+enum Family { kReg, kLane, kCta, kGeneric, kGrp, kBlk };
 
 // interleaved A and X at n = 9..16 (c64): in-place lane groups (k_grp); otherwise the general
 // lane-group kernel (k_lane)
 Family family(int dtype, int n, bool soa) {
     if (n <= reg_max_n(dtype)) return kReg;
     if (soa && dtype == 0 && n <= grp_max_n(dtype)) return kGrp;
+    if (n == 32 || n == 64) return kBlk;
     if (n <= lane_max_n(dtype)) return kLane;
     if (n == 64) return kCta;
     return kGeneric;
 }
 
 const char* family_name(Family f, int dtype, bool ldl) {
-    static const char* names[5][2][2] = {
+    static const char* names[6][2][2] = {
         {{"k_reg<c64,chol>", "k_reg<c64,ldl>"}, {"k_reg<c128,chol>", "k_reg<c128,ldl>"}},
         {{"k_lane<c64,chol>", "k_lane<c64,ldl>"}, {"k_lane<c128,chol>", "k_lane<c128,ldl>"}},
         {{"k_cta64<c64,chol>", "k_cta64<c64,ldl>"}, {"k_cta64<c128,chol>", "k_cta64<c128,ldl>"}},
         {{"k_generic<c64,chol>", "k_generic<c64,ldl>"}, {"k_generic<c128,chol>", "k_generic<c128,ldl>"}},
         {{"k_grp<c64,chol>", "k_grp<c64,ldl>"}, {"k_grp<c128,chol>", "k_grp<c128,ldl>"}},
+        {{"k_blk<c64,chol>", "k_blk<c64,ldl>"}, {"k_blk<c128,chol>", "k_blk<c128,ldl>"}},
     };
     return names[f][dtype][ldl ? 1 : 0];
 }
@@ -94,6 +96,7 @@ int run(int dtype, bool ldl, const LaunchArgs& c) {
     switch (family(dtype, c.n, soa)) {
         case kReg: rc = launch_reg(dtype, ldl, c); break;
         case kGrp: rc = launch_grp(dtype, ldl, c); break;
+        case kBlk: rc = launch_blk(dtype, ldl, c); break;
         case kLane: rc = launch_lane(dtype, ldl, c); break;
         case kCta: rc = launch_cta(dtype, ldl, c); break;
         case kGeneric: break;

@@ -154,20 +154,29 @@ __device__ __forceinline__ void pmac_cb(PAcc<float>& c, const PMul<float>& m, fl
 }
 #endif
 
-// Split accumulator for a MAC whose shared operand is the STREAMED one: acc += r * x with r the
-// pair (r.re, r.im) as loaded and x broadcast per component.  fp32: the two partial sums
-// a = sum x.re * r and b = sum x.im * r are two FFMA2 with no operand rearrangement at all;
-// the value is a + i*b = (a.re - b.im, a.im + b.re), formed once at the end.  fp64: one cfma.
+// Split accumulator for a MAC whose shared operand is the STREAMED one: smac(acc, r, x) with
+// r the pair (r.re, r.im) as loaded and x broadcast per component keeps a = sum x.re * r and
+// b = sum x.im * r (fp32: two FFMA2 with no operand rearrangement at all; fp64: four DFMA).
+//   sval(acc)       = sum r x        = a + i b
+//   sval_conjr(acc) = sum conj(r) x  = conj(sum r conj(x)) = conj(a - i b)
 template <typename T> struct SAcc;
-template <> struct SAcc<double> { double2 v; };
-__device__ __forceinline__ void sacc_zero(SAcc<double>& c) { c.v = make_double2(0.0, 0.0); }
-__device__ __forceinline__ void smac(SAcc<double>& c, double2 r, double2 x) { cfma(c.v, r, x); }
-__device__ __forceinline__ double2 sval(const SAcc<double>& c) { return c.v; }
+template <> struct SAcc<double> { double2 a, b; };
+__device__ __forceinline__ void sacc_zero(SAcc<double>& c) { c.a = make_double2(0.0, 0.0); c.b = c.a; }
+__device__ __forceinline__ void smac(SAcc<double>& c, double2 r, double2 x) {
+    c.a.x = fma(x.x, r.x, c.a.x); c.a.y = fma(x.x, r.y, c.a.y);
+    c.b.x = fma(x.y, r.x, c.b.x); c.b.y = fma(x.y, r.y, c.b.y);
+}
+__device__ __forceinline__ double2 sval(const SAcc<double>& c) { return make_double2(c.a.x - c.b.y, c.a.y + c.b.x); }
+__device__ __forceinline__ double2 sval_conjr(const SAcc<double>& c) { return make_double2(c.a.x + c.b.y, c.b.x - c.a.y); }
 #ifdef HPDINV_NO_FFMA2
-template <> struct SAcc<float> { float2 v; };
-__device__ __forceinline__ void sacc_zero(SAcc<float>& c) { c.v = make_float2(0.f, 0.f); }
-__device__ __forceinline__ void smac(SAcc<float>& c, float2 r, float2 x) { cfma(c.v, r, x); }
-__device__ __forceinline__ float2 sval(const SAcc<float>& c) { return c.v; }
+template <> struct SAcc<float> { float2 a, b; };
+__device__ __forceinline__ void sacc_zero(SAcc<float>& c) { c.a = make_float2(0.f, 0.f); c.b = c.a; }
+__device__ __forceinline__ void smac(SAcc<float>& c, float2 r, float2 x) {
+    c.a.x = fmaf(x.x, r.x, c.a.x); c.a.y = fmaf(x.x, r.y, c.a.y);
+    c.b.x = fmaf(x.y, r.x, c.b.x); c.b.y = fmaf(x.y, r.y, c.b.y);
+}
+__device__ __forceinline__ float2 sval(const SAcc<float>& c) { return make_float2(c.a.x - c.b.y, c.a.y + c.b.x); }
+__device__ __forceinline__ float2 sval_conjr(const SAcc<float>& c) { return make_float2(c.a.x + c.b.y, c.b.x - c.a.y); }
 #else
 template <> struct SAcc<float> { unsigned long long a, b; };
 __device__ __forceinline__ void sacc_zero(SAcc<float>& c) { c.a = 0ull; c.b = 0ull; }
@@ -181,6 +190,12 @@ __device__ __forceinline__ float2 sval(const SAcc<float>& c) {
     upk2(c.a, ax, ay);
     upk2(c.b, bx, by);
     return make_float2(ax - by, ay + bx);
+}
+__device__ __forceinline__ float2 sval_conjr(const SAcc<float>& c) {
+    float ax, ay, bx, by;
+    upk2(c.a, ax, ay);
+    upk2(c.b, bx, by);
+    return make_float2(ax + by, bx - ay);
 }
 #endif
 
@@ -222,6 +237,30 @@ __device__ __forceinline__ float rcp_nr(float t) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(t));
     const float e = fmaf(-t, y, 1.0f);
     return fmaf(y, e, y);
+}
+
+// Pivot reciprocals of the blocked kernels: hardware approximation refined by Newton steps
+// (one for fp32, two for fp64), and exactly 1 when the operand is exactly 1 (the exact integer
+// families stay bit-exact; R9).  1/sqrt(t) for Cholesky, 1/t for LDL.
+__device__ __forceinline__ float rsqrt_fast(float t) { return t == 1.0f ? 1.0f : rsqrt_nr(t); }
+__device__ __forceinline__ float rcp_fast(float t) { return t == 1.0f ? 1.0f : rcp_nr(t); }
+__device__ __forceinline__ double rsqrt_fast(double t) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(t));
+    double e = fma(-t * y, y, 1.0);
+    y = fma(0.5 * y, e, y);
+    e = fma(-t * y, y, 1.0);
+    y = fma(0.5 * y, e, y);
+    return t == 1.0 ? 1.0 : y;
+}
+__device__ __forceinline__ double rcp_fast(double t) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(t));
+    double e = fma(-t, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-t, y, 1.0);
+    y = fma(y, e, y);
+    return t == 1.0 ? 1.0 : y;
 }
 
 // Packed upper-triangle index, row-major: (i, j), i <= j, of an n x n matrix.

@@ -26,6 +26,7 @@ int launch_lane(int dtype, bool ldl, const LaunchArgs& a);      // k_lane_c64.cu
 int launch_generic(int dtype, bool ldl, const LaunchArgs& a);   // k_generic.cu
 int launch_cta(int dtype, bool ldl, const LaunchArgs& a);       // k_cta64.cu (n = 64)
 int launch_grp(int dtype, bool ldl, const LaunchArgs& a);       // k_grp.cu (interleaved, c64 9..16)
+int launch_blk(int dtype, bool ldl, const LaunchArgs& a);       // k_blk.cu (n = 32, 64)
 
 // Largest n of each family per dtype (0 = c64, 1 = c128).
 constexpr int reg_max_n(int dtype) { return dtype == 0 ? 8 : 6; }
