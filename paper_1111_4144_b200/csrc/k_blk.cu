@@ -22,14 +22,24 @@ static int launch_blk_t(const LaunchArgs& a) {
     return 0;
 }
 
+#ifndef HPDINV_BLK_NB32
+#define HPDINV_BLK_NB32 8      // panel height at n = 32
+#endif
+#ifndef HPDINV_BLK_NB64
+#define HPDINV_BLK_NB64 8      // panel height at n = 64
+#endif
+#ifndef HPDINV_BLK_NT64
+#define HPDINV_BLK_NT64 128    // threads per matrix at n = 64
+#endif
+
 template <bool LDL>
 static int launch_blk_m(int dtype, const LaunchArgs& a) {
     if (dtype == 0) {
-        if (a.n == 32) return launch_blk_t<float, 32, 8, LDL, 32, 2>(a);
-        if (a.n == 64) return launch_blk_t<float, 64, 8, LDL, 128, 2>(a);
+        if (a.n == 32) return launch_blk_t<float, 32, HPDINV_BLK_NB32, LDL, 32, 2>(a);
+        if (a.n == 64) return launch_blk_t<float, 64, HPDINV_BLK_NB64, LDL, HPDINV_BLK_NT64, 2>(a);
     } else {
-        if (a.n == 32) return launch_blk_t<double, 32, 8, LDL, 32, 2>(a);
-        if (a.n == 64) return launch_blk_t<double, 64, 8, LDL, 128, 2>(a);
+        if (a.n == 32) return launch_blk_t<double, 32, HPDINV_BLK_NB32, LDL, 32, 2>(a);
+        if (a.n == 64) return launch_blk_t<double, 64, HPDINV_BLK_NB64, LDL, HPDINV_BLK_NT64, 2>(a);
     }
     return kNoKernel;
 }

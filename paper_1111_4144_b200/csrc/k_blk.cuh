@@ -8,14 +8,14 @@
 //                   mirror x_jk = conj(x_kj) of X (written by the inversion once R_KT is used).
 // Factor (eqs. 3-4 / 10-11), panels K = [k0, k0+NB) in ascending order (Crout / left-looking):
 //   F1  P_ij = a_ij - sum_{k<k0} conj(u_ki) r_kj  for i in K, j in [k0, n)     (GEMM, k ascending)
-//   F2a warp 0 factors the NB x NB diagonal block of P (lane = column, right-looking, shuffles)
+//   F2a one warp factors the NB x NB diagonal block of P (lane = column, right-looking)
 //   F2b column-parallel panel solve of rows K for the columns j >= k0+NB (NB-step substitution)
 // Proposed inversion (eqs. 20-24 / 25-29) in the blocked order of SURVEY App. A.2, panels
 // from the bottom, T = [k0+NB, n) already inverted:
 //   I1  C_kj = sum_{m in T} r_km x~_mj        (GEMM over the full Hermitian X_TT)
 //   I2  x_kj = -(1/r_kk)(C_kj + sum_{m in K, m>k} r_km x_mj), j in T, rows k bottom-up
 //   I3  V_kj = sum_{m in T} r_km conj(x_jm)   for k <= j in K (the x~_mj, m in T, of the block)
-//   I4  warp 0: the NB x NB diagonal block by the unblocked recursion with V added
+//   I4  one warp: the NB x NB diagonal block by the unblocked recursion with V added
 // S5 copies W (= X, both halves, x_ji = conj(x_ij) bit for bit, Im x_ii = +0) to global memory.
 #pragma once
 #include "cplx.cuh"
@@ -25,6 +25,7 @@ namespace hpdinv {
 template <typename T, int N, int NB, int NT, int RT>
 struct BlkShape {
     static constexpr int LDW = N + 1;                 // odd row stride: column reads spread banks
+    static constexpr int MINB = (NT >= 256) ? 3 : 1;  // 8-warp CTAs: registers for 3 CTAs/SM
     static constexpr int NBLK = N / NB;
     static constexpr int PR = NB / RT;                // row groups of a GEMM tile grid
     static constexpr int Q = NT / PR;                 // column groups
@@ -38,6 +39,20 @@ struct BlkShape {
 };
 
 namespace blk {
+#ifdef HPDINV_BLK_PROF
+__device__ unsigned long long g_prof[16];      // per-phase cycles of thread 0, summed over CTAs
+#define BLK_PHASE(id)                                             \
+    do {                                                          \
+        if (threadIdx.x == 0) {                                   \
+            const long long t_ = clock64();                       \
+            prof_[prof_cur_] += t_ - prof_t_;                     \
+            prof_t_ = t_;                                         \
+            prof_cur_ = (id);                                     \
+        }                                                         \
+    } while (0)
+#else
+#define BLK_PHASE(id) do {} while (0)
+#endif
 __device__ __forceinline__ void cp_async_elem(void* dst, const void* src, int bytes) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
     if (bytes == 8)
@@ -179,7 +194,7 @@ __device__ __forceinline__ void i1(cplx<T>* W, int k0, int t0, int p, int q) {
 }  // namespace blk
 
 template <typename T, int N, int NB, bool LDL, int NT, int RT>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, BlkShape<T, N, NB, NT, RT>::MINB)
 k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
       cplx<T>* X, int64_t sXm, int64_t sXe, int32_t* __restrict__ info)
 {
@@ -195,9 +210,17 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
 #define WE(i, j) W[(i) * LDW + (j)]
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // the warp that runs the serial diagonal-block phases rotates with the CTA index, so the
+    // co-resident CTAs' serial warps sit on different SM sub-partitions (warp w -> SMSP w % 4)
+    const int swarp = int(blockIdx.x % unsigned(NT / 32));
     const int64_t b = blockIdx.x;
     const V* Ab = A + b * sAm;
 
+#ifdef HPDINV_BLK_PROF
+    long long prof_[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // F1 F2a F2b I1 I2 I3 I4 S5 - S1
+    long long prof_t_ = clock64();
+    int prof_cur_ = 9;                                  // 9 = S1 (load)
+#endif
     // ------------------------------------------------------------------ S1: upper(A) -> W
     for (int e = tid; e < N * N; e += NT) {
         const int i = e / N, j = e - i * N;
@@ -213,6 +236,7 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
     // ============================================================== factorisation, panels up
 #pragma unroll 1
     for (int k0 = 0; k0 < N; k0 += NB) {
+        BLK_PHASE(0);
         // ---- F1: P = A_K,[k0,n) - U_{<k0,K}^H R_{<k0,[k0,n)}  (k ascending, as in eqs. 3-4)
         if (k0 > 0) {
             const int ct = (N - k0 + Q - 1) / Q;     // columns per thread for this panel width
@@ -221,9 +245,10 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
             else blk::f1<T, N, LDW, RT, CT>(W, k0, p, q);
         }
         __syncthreads();
-        // ---- F2a: diagonal block, warp 0, lane l owns column k0 + l; row i of U is broadcast
+        BLK_PHASE(1);
+        // ---- F2a: diagonal block, warp swarp, lane l owns column k0 + l; row i of U is broadcast
         //      through shared memory, the pivot by one shuffle
-        if (warp == 0) {
+        if (warp == swarp) {
             const int l = lane < NB ? lane : NB - 1;
             V pc[NB];
 #pragma unroll
@@ -252,6 +277,7 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
             if (lane == 0 && bad_first && s_inf == 0) s_inf = bad_first;
         }
         __syncthreads();
+        BLK_PHASE(2);
         // ---- F2b: rows K of the columns j >= k0 + NB (forward substitution through R_KK^H)
         {
             const int j = k0 + NB + tid;
@@ -280,6 +306,7 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
 #pragma unroll 1
     for (int k0 = N - NB; k0 >= 0; k0 -= NB) {
         const int t0 = k0 + NB;                       // T = [t0, n)
+        BLK_PHASE(3);
         // ---- I1: C = R_KT X_TT into the upper K x T block (R_KT's upper copy is dead)
         if (t0 < N) {
             const int ct = (N - t0 + Q - 1) / Q;
@@ -288,6 +315,7 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
             else blk::i1<T, N, LDW, RT, CT>(W, k0, t0, p, q);
         }
         __syncthreads();
+        BLK_PHASE(4);
         // ---- I2: rows K of the columns j in T, bottom-up (x_mj, m in K, stays in registers)
         V xk[NB];
         {
@@ -297,15 +325,17 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
                 for (int kk = NB - 1; kk >= 0; kk--) {
                     const int k = k0 + kk;
                     V s = WE(k, j);                                            // C_kj
+                    // m descending: the term of the row just computed (m = kk+1) comes last, so
+                    // the rest of the sum overlaps the previous row's latency
 #pragma unroll
-                    for (int m = 0; m < NB; m++)
-                        if (m > kk) cfma(s, WE(k0 + m, k), xk[m]);              // r_km (lower) x_mj
+                    for (int m = NB - 1; m > kk; m--) cfma(s, WE(k0 + m, k), xk[m]);   // r_km x_mj
                     xk[kk] = LDL ? mk<T>(-s.x, -s.y) : cscale(s, -invs[k]);
                     WE(k, j) = xk[kk];
                 }
             }
         }
         __syncthreads();
+        BLK_PHASE(5);
         // ---- I3: V_kj = sum_{m in T} r_km conj(x_jm), k, j in K, into the scratch Vs; SPL
         //      adjacent threads split the sum over m and combine by shuffles
         if (t0 < N) {
@@ -315,8 +345,15 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
 #pragma unroll 1
             for (int o = tid / SPL; o < NB * NB; o += OPS) {
                 const int kk = o / NB, jj = o - kk * NB;
-                V sv = czero<T>();
-                for (int m = t0 + part; m < N; m += SPL) cfma_cb(sv, WE(m, k0 + kk), WE(k0 + jj, m));
+                V sv = czero<T>(), sv2 = czero<T>();                          // two chains
+                int m = t0 + part;
+                for (; m + SPL < N; m += 2 * SPL) {
+                    cfma_cb(sv, WE(m, k0 + kk), WE(k0 + jj, m));
+                    cfma_cb(sv2, WE(m + SPL, k0 + kk), WE(k0 + jj, m + SPL));
+                }
+                if (m < N) cfma_cb(sv, WE(m, k0 + kk), WE(k0 + jj, m));
+                sv.x += sv2.x;
+                sv.y += sv2.y;
 #pragma unroll
                 for (int off = 1; off < SPL; off <<= 1) {
                     sv.x += __shfl_xor_sync(0xffffffffu, sv.x, off);
@@ -334,10 +371,11 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
                 for (int kk = 0; kk < NB; kk++) WE(j, k0 + kk) = conjz(xk[kk]);
             }
         }
-        // ---- I4: the diagonal block, warp 0, lane l owns column k0 + l (full column in registers);
+        BLK_PHASE(6);
+        // ---- I4: the diagonal block, warp swarp, lane l owns column k0 + l (full column in registers);
         //      row k of X goes to W at once (it overwrites the dead upper U row k) and the owner
         //      of column k reads it back as its lower part (the mirror) and forms x_kk
-        if (warp == 0) {
+        if (warp == swarp) {
             const int l = lane < NB ? lane : NB - 1;
             const int j = k0 + l;
             V xc[NB];
@@ -349,21 +387,23 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
                 const T ik = invs[k];
                 V sv = (t0 < N) ? Vs[kk * NB + l] : czero<T>();                 // V_kj
 #pragma unroll
-                for (int m = 0; m < NB; m++)
-                    if (m > kk) cfma(sv, WE(k0 + m, k), xc[m]);                 // r_km x~_mj
+                for (int m = NB - 1; m > kk; m--) cfma(sv, WE(k0 + m, k), xc[m]);   // r_km x~_mj
                 const V xv = LDL ? mk<T>(-sv.x, -sv.y) : cscale(sv, -ik);
                 if (lane > kk && lane < NB) { xc[kk] = xv; WE(k, j) = xv; }
                 __syncwarp();
                 if (lane == kk) {
                     T pd = (t0 < N) ? Vs[kk * NB + kk].x : T(0);                // Re V_kk
+                    T pd2 = T(0);                                                // two chains
 #pragma unroll
                     for (int m = 0; m < NB; m++) {
                         if (m > kk) {
                             const V xkm = WE(k, k0 + m);
-                            pd = re_dot_conj(pd, WE(k0 + m, k), xkm);            // Re r_km conj(x_km)
+                            if ((m - kk) & 1) pd = re_dot_conj(pd, WE(k0 + m, k), xkm);   // Re r_km conj(x_km)
+                            else pd2 = re_dot_conj(pd2, WE(k0 + m, k), xkm);
                             xc[m] = conjz(xkm);
                         }
                     }
+                    pd += pd2;
                     xc[kk] = mk<T>(LDL ? ik - pd : ik * (ik - pd), T(0));
                 }
             }
@@ -377,6 +417,7 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
     }
     }
 
+    BLK_PHASE(7);
     // ------------------------------------------------------------------ S5: store X
     V* Xb = X + b * sXm;
     const T nan = qnan<T>();
@@ -387,6 +428,11 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
         Xb[int64_t(e) * sXe] = v;
     }
     if (tid == 0) info[b] = inf;
+#ifdef HPDINV_BLK_PROF
+    BLK_PHASE(8);
+    if (tid == 0)
+        for (int i = 0; i < 10; i++) atomicAdd(&blk::g_prof[i], (unsigned long long)prof_[i]);
+#endif
 #undef WE
 }
 
