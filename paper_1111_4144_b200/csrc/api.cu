@@ -55,6 +55,7 @@ enum Family { kReg, kLane, kCta, kGeneric, kGrp, kBlk };
 Family family(int dtype, int n, bool soa) {
     if (n <= reg_max_n(dtype)) return kReg;
     if (soa && dtype == 0 && n <= grp_max_n(dtype)) return kGrp;
+    if (dtype == 0 && n == 32) return kGrp;            // 16 lanes per matrix, either layout
     if (n == 32 || n == 64) return kBlk;
     if (n <= lane_max_n(dtype)) return kLane;
     if (n == 64) return kCta;

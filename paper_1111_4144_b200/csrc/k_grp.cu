@@ -11,17 +11,18 @@ static int launch_grp_t(const LaunchArgs& a) {
     fn_t fn = nullptr;
     size_t smem = 0;
     int mpc = 1, threads = 0;
-#define HPDINV_GRP(NN)                          \
-    case NN:                                    \
-        fn = k_grp<T, NN, LDL>;                 \
-        smem = GrpShape<T, NN>::smem_bytes;     \
-        mpc = GrpShape<T, NN>::MPC;             \
-        threads = GrpShape<T, NN>::THREADS;     \
+#define HPDINV_GRP(NN, GG)                          \
+    case NN:                                        \
+        fn = k_grp<T, NN, GG, LDL>;                 \
+        smem = GrpShape<T, NN, GG>::smem_bytes;     \
+        mpc = GrpShape<T, NN, GG>::MPC;             \
+        threads = GrpShape<T, NN, GG>::THREADS;     \
         break;
     if constexpr (sizeof(T) == 4) {
         switch (a.n) {
-            HPDINV_GRP(9) HPDINV_GRP(10) HPDINV_GRP(11) HPDINV_GRP(12)
-            HPDINV_GRP(13) HPDINV_GRP(14) HPDINV_GRP(15) HPDINV_GRP(16)
+            HPDINV_GRP(9, 4) HPDINV_GRP(10, 4) HPDINV_GRP(11, 4) HPDINV_GRP(12, 4)
+            HPDINV_GRP(13, 4) HPDINV_GRP(14, 4) HPDINV_GRP(15, 4) HPDINV_GRP(16, 4)
+            HPDINV_GRP(32, 16)
             default: break;
         }
     }

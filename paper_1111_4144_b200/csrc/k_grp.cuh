@@ -1,5 +1,6 @@
-// k_grp.cuh -- G = 4 lanes per matrix, 8 matrices per warp, every column held IN PLACE in
-// registers: the config-3 kernel (n = 16, complex64, interleaved, 2^22 matrices).
+// k_grp.cuh -- G lanes per matrix (G = 4 at n <= 16, 8 matrices per warp; G = 16 at n = 32, 2 per
+// warp), every column held IN PLACE in registers: the config-3 kernel (n = 16, complex64,
+// interleaved, 2^22 matrices) and the config-5 kernel (n = 32, complex64, LDL, contiguous).
 //
 // Design (why not one matrix per thread): the fully unrolled per-thread code of an n = 16
 // matrix (~9.5k instructions, 150 KB) thrashes the instruction cache ("no_instruction" was the
@@ -34,18 +35,17 @@
 
 namespace hpdinv {
 
-template <typename T, int N>
+template <typename T, int N, int G_>
 struct GrpShape {
-    static constexpr int G = 4;                       // lanes per matrix
+    static constexpr int G = G_;                      // lanes per matrix
     static constexpr int C = (N + G - 1) / G;         // columns per lane
     static constexpr int MPW = 32 / G;                // matrices per warp
     static constexpr int WARPS = 4;
     static constexpr int THREADS = 32 * WARPS;
     static constexpr int MPC = MPW * WARPS;           // matrices per CTA
-#ifndef HPDINV_GRP_MINB
-#define HPDINV_GRP_MINB 3
-#endif
-    static constexpr int MIN_BLOCKS = HPDINV_GRP_MINB;  // 3: caps ptxas at 170 registers, 12 warps/SM
+    // n <= 16: 3 CTAs/SM caps ptxas at 170 registers (12 warps/SM); n = 32 (two 32-row columns
+    // per lane) runs 8 warps/SM with up to 255 registers instead of spilling (measured faster)
+    static constexpr int MIN_BLOCKS = N <= 16 ? 3 : 2;
     static constexpr int P = sizeof(T) == 4 ? 2 : 1;  // complex elements per 16-byte load
     // packed row store: row i holds j = i..n-1 at offset roff(i) + (j - i), 16-byte aligned
     __host__ __device__ static constexpr int rlen(int i) { return ((N - i) + P - 1) / P * P; }
@@ -73,12 +73,12 @@ __device__ __forceinline__ void lds_pair(const cplx<T>* p, int o, cplx<T>& e0, c
 }
 }  // namespace grp
 
-template <typename T, int N, bool LDL>
-__global__ void __launch_bounds__(GrpShape<T, N>::THREADS, GrpShape<T, N>::MIN_BLOCKS)
+template <typename T, int N, int GG, bool LDL>
+__global__ void __launch_bounds__(GrpShape<T, N, GG>::THREADS, GrpShape<T, N, GG>::MIN_BLOCKS)
 k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
       cplx<T>* X, int64_t sXm, int64_t sXe, int32_t* __restrict__ info)
 {
-    using Sh = GrpShape<T, N>;
+    using Sh = GrpShape<T, N, GG>;
     using V = cplx<T>;
     constexpr int G = Sh::G, C = Sh::C, P = Sh::P;
     constexpr unsigned FULL = 0xffffffffu;
