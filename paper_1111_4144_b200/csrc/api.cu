@@ -48,7 +48,7 @@ LayoutClass classify(int64_t batch, int n, int64_t sm, int64_t se) {
     return kInvalid;
 }
 
-enum Family { kReg, kLane, kCta, kGeneric, kGrp, kBlk };
+enum Family { kReg, kLane, kGeneric, kGrp, kBlk };
 
 // interleaved A and X at n = 9..16 (c64): in-place lane groups (k_grp); otherwise the general
 // lane-group kernel (k_lane)
@@ -58,15 +58,13 @@ Family family(int dtype, int n, bool soa) {
     if (dtype == 0 && n == 32) return kGrp;            // 16 lanes per matrix, either layout
     if (n == 32 || n == 64) return kBlk;
     if (n <= lane_max_n(dtype)) return kLane;
-    if (n == 64) return kCta;
     return kGeneric;
 }
 
 const char* family_name(Family f, int dtype, bool ldl) {
-    static const char* names[6][2][2] = {
+    static const char* names[5][2][2] = {
         {{"k_reg<c64,chol>", "k_reg<c64,ldl>"}, {"k_reg<c128,chol>", "k_reg<c128,ldl>"}},
         {{"k_lane<c64,chol>", "k_lane<c64,ldl>"}, {"k_lane<c128,chol>", "k_lane<c128,ldl>"}},
-        {{"k_cta64<c64,chol>", "k_cta64<c64,ldl>"}, {"k_cta64<c128,chol>", "k_cta64<c128,ldl>"}},
         {{"k_generic<c64,chol>", "k_generic<c64,ldl>"}, {"k_generic<c128,chol>", "k_generic<c128,ldl>"}},
         {{"k_grp<c64,chol>", "k_grp<c64,ldl>"}, {"k_grp<c128,chol>", "k_grp<c128,ldl>"}},
         {{"k_blk<c64,chol>", "k_blk<c64,ldl>"}, {"k_blk<c128,chol>", "k_blk<c128,ldl>"}},
@@ -99,7 +97,6 @@ int run(int dtype, bool ldl, const LaunchArgs& c) {
         case kGrp: rc = launch_grp(dtype, ldl, c); break;
         case kBlk: rc = launch_blk(dtype, ldl, c); break;
         case kLane: rc = launch_lane(dtype, ldl, c); break;
-        case kCta: rc = launch_cta(dtype, ldl, c); break;
         case kGeneric: break;
     }
     if (rc == kNoKernel && c.n <= lane_max_n(dtype)) rc = launch_lane(dtype, ldl, c);   // k_grp declined

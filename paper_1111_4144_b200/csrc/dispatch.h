@@ -24,7 +24,6 @@ constexpr int kNoKernel = -1000;   // launcher has no instantiation for this n
 int launch_reg(int dtype, bool ldl, const LaunchArgs& a);       // k_reg.cu
 int launch_lane(int dtype, bool ldl, const LaunchArgs& a);      // k_lane_c64.cu / k_lane_c128.cu
 int launch_generic(int dtype, bool ldl, const LaunchArgs& a);   // k_generic.cu
-int launch_cta(int dtype, bool ldl, const LaunchArgs& a);       // k_cta64.cu (n = 64)
 int launch_grp(int dtype, bool ldl, const LaunchArgs& a);       // k_grp.cu (interleaved, c64 9..16)
 int launch_blk(int dtype, bool ldl, const LaunchArgs& a);       // k_blk.cu (n = 32, 64)
 
