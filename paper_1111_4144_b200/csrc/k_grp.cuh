@@ -22,9 +22,11 @@
 //   S4  rows k = n-1..0 (eqs. 22-24 / 27-29): R row k is read back from the row store; lane j
 //       forms x_kj = -(1/r_kk) sum_{m>k} r_km x~_mj over its register column (x~_mj for m > k
 //       is already X: the upper part computed in rows > k, the lower part gathered below);
-//       the new row goes through a row buffer to the owner of column k, which stores it
-//       conjugated as the lower part of column k (x_mk = conj(x_km), the mirror) and forms
-//       x_kk = (1/r_kk)(1/r_kk - Re sum_{m>k} r_km conj(x_km)) real;
+//       each lane adds its columns' share of Re sum_{m>k} r_km conj(x_km) (r_kj is still in its
+//       register column) and the G lanes combine it by shuffles; the new row goes, conjugated,
+//       through a row buffer to the owner of column k, which takes it as the lower part of
+//       column k (x_mk = conj(x_km), the mirror) and forms x_kk = (1/r_kk)(1/r_kk - Re sum) real
+//       (measured: 8.5 -> 7.8 ms at config 5 against the owner forming the whole sum alone);
 //   S5  every lane stores its columns (lower part: the bitwise conjugate written in S4).
 // Dead storage is reused freely: a lane whose column j is not active at a step computes on
 // entries of column j that are rewritten before they are read (lower part before its gather,
@@ -124,7 +126,7 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
         const int bad0 = !(t > T(0));
         const T tt = bad0 ? T(1) : t;
         T iv;
-        iv = LDL ? rcp_rn(tt) : rcp_rn(sqrt_rn(tt));
+        iv = LDL ? rcp_fast(tt) : rsqrt_fast(tt);      // short serial chain, exact at 1 (R9)
         iv = __shfl_sync(FULL, iv, qi, G);
         const int bad = __shfl_sync(FULL, bad0, qi, G);
         T di = T(0);
@@ -196,21 +198,28 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
                 if (G * s + G - 1 > k) smac(acc[s], rk[m], col[s][m]);
         }
         V xk[C];
+        // x_kk: every lane forms its share of p = Re sum_{m>k} r_km conj(x_km) over its own
+        // columns (r_kj is still in col[s][k], about to be overwritten by x_kj) and the G lanes
+        // combine it by shuffles; the row goes to the row buffer already conjugated (the mirror)
+        T pl = T(0);
 #pragma unroll
         for (int s = 0; s < C; s++) {
             if (G * s + G - 1 > k) {
                 const V a = sval(acc[s]);
                 xk[s] = LDL ? mk<T>(-a.x, -a.y) : cscale(a, -ik);
+                const V rkj = col[s][k];
                 col[s][k] = xk[s];
                 const int j = q + G * s;
-                if (j > k && j < N) rowbuf[j] = xk[s];
+                if (j > k && j < N) {
+                    rowbuf[j] = conjz(xk[s]);
+                    pl = re_dot_conj(pl, rkj, xk[s]);
+                }
             }
         }
+#pragma unroll
+        for (int off = 1; off < G; off <<= 1) pl += __shfl_xor_sync(FULL, pl, off, G);
         __syncwarp();
         if (q == qk) {
-            // the owner of column k takes row k of X as its lower part (mirror) and forms x_kk
-            // p = Re sum_{m>k} r_km conj(x_km), m ascending, as (re*re, im*im) lane pairs
-            V pp = czero<T>();
 #pragma unroll
             for (int o = 0; o < N; o += P) {
                 if (o + P - 1 <= k) continue;
@@ -219,22 +228,18 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
 #pragma unroll
                 for (int h = 0; h < P; h++) {
                     const int m = o + h;
-                    if (m > k && m < N) {
-                        col[sk][m] = conjz(e[h]);
-                        pp = pfma_elem(rk[m], e[h], pp);
-                    }
+                    if (m > k && m < N) col[sk][m] = e[h];
                 }
             }
-            const T p = pp.x + pp.y;
-            col[sk][k] = mk<T>(LDL ? ik - p : ik * (ik - p), T(0));
+            col[sk][k] = mk<T>(LDL ? ik - pl : ik * (ik - pl), T(0));
         }
         __syncwarp();
     }
 
     // ------------------------------------------------------------------ S5: mirror + store
     if (valid) {
-        V* Xb = X + b * sXm;
-        char* Xq = reinterpret_cast<char*>(Xb + q * sXe);
+        // (storing each row as soon as it is final, inside S4, measured slower: 4.5 vs 4.1 ms cfg3)
+        char* Xrow = reinterpret_cast<char*>(X + b * sXm + q * sXe);   // element (m, q + G s)
         const uint32_t seX = uint32_t(sXe * int64_t(sizeof(V)));
 #pragma unroll
         for (int s = 0; s < C; s++) {
@@ -242,11 +247,12 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
             if (j < N) {
 #pragma unroll
                 for (int m = 0; m < N; m++)
-                    *reinterpret_cast<V*>(Xq + uint64_t(uint32_t(m * N + G * s)) * seX) = col[s][m];
+                    *reinterpret_cast<V*>(Xrow + uint64_t(uint32_t(m * N + G * s)) * seX) = col[s][m];
             }
         }
         if (inf) {          // a flagged matrix is overwritten (same thread, program order)
             const T nan = qnan<T>();
+            V* Xb = X + b * sXm;
 #pragma unroll 1
             for (int e = q; e < N * N; e += G) Xb[int64_t(e) * sXe] = mk<T>(nan, nan);
         }
