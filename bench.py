@@ -53,13 +53,22 @@ def parse():
 
 
 # ----------------------------------------------------------------------------- helpers
+METRIC_SOLVE = "HPD linear systems solved/sec (SURVEY 8(f) f1: A x = y, eqs. 5-7 / 12-14), 1 B200"
+UNIT_SOLVE = "systems/s"
+
+
 def algorithmic_bytes(cfg: wl.Config) -> int:
-    """Per matrix: read the upper triangle, write all n^2 entries of X and one int32 info."""
+    """Per matrix: read the upper triangle, write all n^2 entries of X and one int32 info
+    (solve: read the upper triangle and y, write x and info)."""
     n, e = cfg.n, cfg.elem_bytes
+    if cfg.task == "solve":
+        return e * (n * (n + 1) // 2 + 2 * n) + 4
     return e * (n * (n + 1) // 2 + n * n) + 4
 
 
-def cmul_per_matrix(n: int) -> int:
+def cmul_per_matrix(n: int, task: str = "inv") -> int:
+    if task == "solve":               # factor (n^3-n)/6 + two substitutions n(n-1)/2 each
+        return (n ** 3 - n) // 6 + n * (n - 1)
     return (n ** 3 - n) // 2          # Table 1 proposed total, exact (SURVEY App. A.3)
 
 
@@ -172,12 +181,24 @@ def run_ours(args, rank, world, local_rank):
     A = wl.generate(cfg, rank * B, B, device=dev, seed=args.seed)   # this rank's slice
     store, view = wl.to_layout(A, cfg.layout)
     del A
-    X = wl.empty_like_layout(view)
     info = torch.empty(B, dtype=torch.int32, device=dev)
-    kernel = hp.kernel_name(cfg.method, cfg.dtype, B, cfg.n, (view.stride(0), view.stride(2)))
+    solve = cfg.task == "solve"
+    metric, unit = (METRIC_SOLVE, UNIT_SOLVE) if solve else (METRIC, UNIT)
+    if solve:
+        Y = wl.generate_rhs(cfg, rank * B, B, device=dev, seed=args.seed)
+        _, yview = wl.vec_layout(Y, cfg.layout)
+        del Y
+        Xv = torch.empty_strided(yview.shape, yview.stride(), dtype=cfg.dtype, device=dev)
+        kernel = hp.solve_kernel_name(cfg.method, cfg.dtype, cfg.n)
 
-    def step():
-        hp.invert(view, cfg.method, X=X, info=info)
+        def step():
+            hp.solve(view, yview, cfg.method, Xv=Xv, info=info)
+    else:
+        X = wl.empty_like_layout(view)
+        kernel = hp.kernel_name(cfg.method, cfg.dtype, B, cfg.n, (view.stride(0), view.stride(2)))
+
+        def step():
+            hp.invert(view, cfg.method, X=X, info=info)
 
     per_step_guess = algorithmic_bytes(cfg) * B / 6.0e12
     steps = args.steps if args.steps is not None else max(20, min(2000, int(0.5 / per_step_guess)))
@@ -220,7 +241,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- end to end through the host-buffer C entry point (H2D + kernel + D2H timed)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not solve:
         A_host = store.cpu().pin_memory()
         if cfg.layout == "soa":
             vh = wl.soa_view(A_host, B, cfg.n)
@@ -265,7 +286,7 @@ def run_ours(args, rank, world, local_rank):
     bytes_launch = algorithmic_bytes(cfg) * B
     mem_s = bytes_launch / (pk["hbm_gbs"] * 1e9)
     fp_tf = fp_peak_tflops(cfg.dtype, pk["sm_max_mhz"])
-    flops_launch = 8.0 * cmul_per_matrix(cfg.n) * B
+    flops_launch = 8.0 * cmul_per_matrix(cfg.n, cfg.task) * B
     fp_s = flops_launch / (fp_tf * 1e12)
     if fp_s > mem_s:
         achieved = flops_launch / (kern_ms / 1e3) / 1e12
@@ -284,7 +305,7 @@ def run_ours(args, rank, world, local_rank):
     bj_bytes = 2 * cfg.elem_bytes * cfg.n ** 2 * B
     bj_t = max(bj_bytes / (pk["hbm_gbs"] * 1e9), fp_s)
     out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+        "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": steps,
         "warmup": warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32" if cfg.dtype == torch.complex64 else "f64",
         "data": "synthetic (seeded, chunk-keyed; BASELINE.json configs recipe)",
@@ -300,6 +321,11 @@ def run_ours(args, rank, world, local_rank):
                                       "bytes": bj_bytes, "note": "BASELINE.json north_star formula"},
         "clocks": clocks, "gpu_launches": steps, "info_nonzero": bad, "e2e": e2e,
     }
+    if solve:
+        out["config"]["task"] = "solve (1 right-hand side per matrix)"
+        out.pop("roofline_baseline_formula")
+        if e2e is None:
+            out["e2e_note"] = "the solve has no host-buffer entry point yet"
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, args, budget_s=args.cpu_seconds, dev=dev)
     return out
@@ -313,20 +339,34 @@ def oracle_sample(cfg: wl.Config, count: int, seed: int, dev):
     return A.cpu().to(torch.complex128).numpy()
 
 
+def oracle_run(cfg: wl.Config, Ah, yh):
+    import oracle
+    if cfg.task == "solve":
+        return oracle.solve_batched(Ah, yh, cfg.method)
+    return oracle.inv_batched(Ah, cfg.method)
+
+
+def oracle_rhs(cfg: wl.Config, count: int, seed: int, dev):
+    if cfg.task != "solve":
+        return None
+    return wl.generate_rhs(cfg, 0, count, device=dev, seed=seed).cpu().to(torch.complex128).numpy()
+
+
 def cpu_baseline(cfg: wl.Config, args, budget_s: float, dev):
     import oracle
     oracle.build()
     cores = oracle.max_threads()
-    Ah = oracle_sample(cfg, min(cfg.batch, 1024), args.seed, dev)
+    n0 = min(cfg.batch, 1024)
+    Ah, yh = oracle_sample(cfg, n0, args.seed, dev), oracle_rhs(cfg, n0, args.seed, dev)
     t0 = time.perf_counter()
-    oracle.inv_batched(Ah, cfg.method)
+    oracle_run(cfg, Ah, yh)
     per = (time.perf_counter() - t0) / Ah.shape[0]
     count = int(min(cfg.batch, max(Ah.shape[0], budget_s / max(per, 1e-9))))
-    Ah = oracle_sample(cfg, count, args.seed, dev)
+    Ah, yh = oracle_sample(cfg, count, args.seed, dev), oracle_rhs(cfg, count, args.seed, dev)
     t0 = time.perf_counter()
-    oracle.inv_batched(Ah, cfg.method)
+    oracle_run(cfg, Ah, yh)
     dt = time.perf_counter() - t0
-    return {"value": count / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": count / dt, "unit": UNIT_SOLVE if cfg.task == "solve" else UNIT, "cores": cores, "kind": "oracle",
             "sample": "first %d of the %d matrices of cfg%d (%s), fp64 C oracle, OpenMP over matrices"
             % (count, cfg.batch, cfg.cid, cfg.method), "seconds": dt,
             "cpu": _cpu_model()}
@@ -350,34 +390,37 @@ def run_reference(args, rank, world):
     steps = args.steps if args.steps is not None else 5
     warmup = args.warmup if args.warmup is not None else 1
     # each step: a bounded sample sized so the whole run takes ~2-3 minutes
-    Ah = oracle_sample(cfg, min(cfg.batch, 512), args.seed, dev)
+    n0 = min(cfg.batch, 512)
+    Ah, yh = oracle_sample(cfg, n0, args.seed, dev), oracle_rhs(cfg, n0, args.seed, dev)
     t0 = time.perf_counter()
-    oracle.inv_batched(Ah, cfg.method)
+    oracle_run(cfg, Ah, yh)
     per = (time.perf_counter() - t0) / Ah.shape[0]
     per_step_s = max(0.2, min(20.0, 150.0 / max(1, steps + warmup)))
     count = int(min(cfg.batch, max(64, per_step_s / max(per, 1e-9))))
-    Ah = oracle_sample(cfg, count, args.seed, dev)
+    Ah, yh = oracle_sample(cfg, count, args.seed, dev), oracle_rhs(cfg, count, args.seed, dev)
     for _ in range(warmup):
-        oracle.inv_batched(Ah, cfg.method)
+        oracle_run(cfg, Ah, yh)
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
-        X, info = oracle.inv_batched(Ah, cfg.method)
+        X, info = oracle_run(cfg, Ah, yh)
         times.append(time.perf_counter() - t0)
     ms = 1e3 * sum(times) / len(times)
     value = count / (ms / 1e3)
     cores = oracle.max_threads()
+    solve = cfg.task == "solve"
+    UNITX = UNIT_SOLVE if solve else UNIT
     return {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "impl": "reference", "metric": METRIC_SOLVE if solve else METRIC, "value": value, "unit": UNITX, "n_gpus": world,
         "steps": steps, "warmup": warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "cfg%d: %s" % (cfg.cid, cfg.desc), "n": cfg.n,
                    "batch_per_gpu": cfg.batch, "method": cfg.method, "layout": cfg.layout,
                    "sample_per_step": count},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": UNITX, "cores": cores, "kind": "oracle",
                          "sample": "first %d of the %d matrices of cfg%d per step" % (count, cfg.batch, cfg.cid),
                          "cpu": _cpu_model()},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": value, "unit": UNITX, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "info_nonzero": int((info != 0).sum()),
     }
 

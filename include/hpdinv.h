@@ -94,6 +94,46 @@ int ldl_inv_batched_c128(int64_t batch, int n,
                          int32_t *info, cudaStream_t stream);
 
 /* ---------------------------------------------------------------------------------------
+ * Batched linear solve with the same factorisation.
+ *
+ * Solves A_b x_b = y_b for every b: Cholesky per eqs. (5)-(7), P:49-61 (R* b = y by forward
+ * substitution, then R x = b), LDL per eqs. (12)-(14), P:87-99 (R* D b = y, then R x = b with
+ * R unit upper).  One right-hand side per matrix, as in the paper (x, y in C^{N x 1}).
+ *   A: as for the inversion (only the upper triangle and Re a_ii are read; same layouts).
+ *   Y, Xv: vector element i of system b at base[b*stride_mat + i*stride_elem]; accepted
+ *     layouts: interleaved (stride_mat = 1, stride_elem >= batch) or contiguous
+ *     (stride_elem = 1, stride_mat >= n); n = 1: any stride_mat >= 1.  Xv may alias Y with
+ *     identical strides; it may not overlap A.
+ *   info: as for the inversion; Xv_b is NaN when info[b] != 0.
+ * Returns 0, -k for invalid argument k (1-based: 1 batch, 2 n, 3 A, 4/5 A strides, 6 Y,
+ * 7/8 Y strides, 9 Xv, 10/11 Xv strides, 12 info), or a cudaError_t from the launch.
+ * Asynchronous, stream-ordered; no allocation.  Kernels: one system per thread with the
+ * triangle in registers for n <= 8 (c64) / n <= 6 (c128), else one system per CTA. */
+int chol_solve_batched_c64(int64_t batch, int n,
+                           const cuFloatComplex *A, int64_t strideA_mat, int64_t strideA_elem,
+                           const cuFloatComplex *Y, int64_t strideY_mat, int64_t strideY_elem,
+                           cuFloatComplex *Xv, int64_t strideX_mat, int64_t strideX_elem,
+                           int32_t *info, cudaStream_t stream);
+int chol_solve_batched_c128(int64_t batch, int n,
+                            const cuDoubleComplex *A, int64_t strideA_mat, int64_t strideA_elem,
+                            const cuDoubleComplex *Y, int64_t strideY_mat, int64_t strideY_elem,
+                            cuDoubleComplex *Xv, int64_t strideX_mat, int64_t strideX_elem,
+                            int32_t *info, cudaStream_t stream);
+int ldl_solve_batched_c64(int64_t batch, int n,
+                          const cuFloatComplex *A, int64_t strideA_mat, int64_t strideA_elem,
+                          const cuFloatComplex *Y, int64_t strideY_mat, int64_t strideY_elem,
+                          cuFloatComplex *Xv, int64_t strideX_mat, int64_t strideX_elem,
+                          int32_t *info, cudaStream_t stream);
+int ldl_solve_batched_c128(int64_t batch, int n,
+                           const cuDoubleComplex *A, int64_t strideA_mat, int64_t strideA_elem,
+                           const cuDoubleComplex *Y, int64_t strideY_mat, int64_t strideY_elem,
+                           cuDoubleComplex *Xv, int64_t strideX_mat, int64_t strideX_elem,
+                           int32_t *info, cudaStream_t stream);
+
+/* Name of the solve kernel the dispatcher would launch (static string; NULL if invalid). */
+const char *hpdinv_solve_kernel_name(int method, int dtype, int n);
+
+/* ---------------------------------------------------------------------------------------
  * Host-buffer entry point (end-to-end use from host memory).
  *
  * hpdinv_inv_host runs the same hot path on matrices that live in HOST memory (pinned

@@ -19,7 +19,8 @@ from ._lib import EXPORTS, HpdinvError, lib  # noqa: F401
 
 __all__ = [
     "chol_inv_batched_c64", "chol_inv_batched_c128", "ldl_inv_batched_c64",
-    "ldl_inv_batched_c128", "invert", "invert_host", "host_workspace_bytes", "kernel_name", "version", "HpdinvError",
+    "ldl_inv_batched_c128", "chol_solve_batched_c64", "chol_solve_batched_c128",
+    "ldl_solve_batched_c64", "ldl_solve_batched_c128", "solve", "solve_kernel_name", "invert", "invert_host", "host_workspace_bytes", "kernel_name", "version", "HpdinvError",
 ]
 
 
@@ -94,6 +95,79 @@ _DISPATCH = {
 def invert(A, method: str = "chol", X=None, info=None, stream=None):
     """Dispatch on (method, A.dtype) to the matching C entry point."""
     return _DISPATCH[(method, A.dtype)](A, X, info, stream)
+
+
+def _vstrides(v: torch.Tensor) -> Tuple[int, int]:
+    if v.dim() != 2:
+        raise ValueError("expected a (batch, n) tensor, got shape %s" % (tuple(v.shape),))
+    return v.stride(0), v.stride(1)
+
+
+def _call_solve(fname: str, dtype: torch.dtype, A, Y, Xv, info, stream):
+    for t, nm in ((A, "A"), (Y, "Y")):
+        if t.dtype != dtype:
+            raise TypeError("%s expects %s for %s, got %s" % (fname, dtype, nm, t.dtype))
+        if not t.is_cuda:
+            raise ValueError("%s: %s must be a CUDA tensor (no CPU path exists)" % (fname, nm))
+    batch, n = A.shape[0], A.shape[1]
+    if tuple(Y.shape) != (batch, n):
+        raise ValueError("Y must have shape (batch, n)")
+    sAm, sAe = _strides(A)
+    sYm, sYe = _vstrides(Y)
+    if Xv is None:
+        Xv = torch.empty_strided(Y.shape, Y.stride(), dtype=dtype, device=Y.device)
+    sXm, sXe = _vstrides(Xv)
+    if info is None:
+        info = torch.empty(batch, dtype=torch.int32, device=A.device)
+    if info.dtype != torch.int32 or info.numel() < batch or not info.is_contiguous():
+        raise ValueError("info must be a contiguous int32 tensor of length >= batch")
+    rc = getattr(lib(), fname)(batch, n, ctypes.c_void_p(A.data_ptr()), sAm, sAe,
+                               ctypes.c_void_p(Y.data_ptr()), sYm, sYe,
+                               ctypes.c_void_p(Xv.data_ptr()), sXm, sXe,
+                               ctypes.c_void_p(info.data_ptr()), ctypes.c_void_p(_stream_handle(stream)))
+    if rc < 0:
+        raise ValueError("%s rejected argument %d" % (fname, -rc))
+    if rc > 0:
+        raise HpdinvError("%s: CUDA error %d at launch" % (fname, rc))
+    return Xv, info
+
+
+def chol_solve_batched_c64(A, Y, Xv=None, info=None, stream=None):
+    """A x = y by Cholesky, eqs. (5)-(7), complex64.  Y, Xv: (batch, n) views."""
+    return _call_solve("chol_solve_batched_c64", torch.complex64, A, Y, Xv, info, stream)
+
+
+def chol_solve_batched_c128(A, Y, Xv=None, info=None, stream=None):
+    """A x = y by Cholesky, eqs. (5)-(7), complex128."""
+    return _call_solve("chol_solve_batched_c128", torch.complex128, A, Y, Xv, info, stream)
+
+
+def ldl_solve_batched_c64(A, Y, Xv=None, info=None, stream=None):
+    """A x = y by LDL, eqs. (12)-(14), complex64."""
+    return _call_solve("ldl_solve_batched_c64", torch.complex64, A, Y, Xv, info, stream)
+
+
+def ldl_solve_batched_c128(A, Y, Xv=None, info=None, stream=None):
+    """A x = y by LDL, eqs. (12)-(14), complex128."""
+    return _call_solve("ldl_solve_batched_c128", torch.complex128, A, Y, Xv, info, stream)
+
+
+_SOLVE = {
+    ("chol", torch.complex64): chol_solve_batched_c64,
+    ("chol", torch.complex128): chol_solve_batched_c128,
+    ("ldl", torch.complex64): ldl_solve_batched_c64,
+    ("ldl", torch.complex128): ldl_solve_batched_c128,
+}
+
+
+def solve(A, Y, method: str = "chol", Xv=None, info=None, stream=None):
+    """Batched A_b x_b = y_b with the same factorisation."""
+    return _SOLVE[(method, A.dtype)](A, Y, Xv, info, stream)
+
+
+def solve_kernel_name(method: str, dtype: torch.dtype, n: int):
+    r = lib().hpdinv_solve_kernel_name({"chol": 0, "ldl": 1}[method], {torch.complex64: 0, torch.complex128: 1}[dtype], n)
+    return r.decode() if r else None
 
 
 def host_workspace_bytes(dtype: torch.dtype, n: int, chunk: int) -> int:

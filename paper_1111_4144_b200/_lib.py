@@ -29,6 +29,14 @@ def lib() -> ctypes.CDLL:
         f = getattr(L, name)
         f.restype = I
         f.argtypes = inv_args
+    solve_args = [I64, I, P, I64, I64, P, I64, I64, P, I64, I64, P, P]
+    for name in ("chol_solve_batched_c64", "chol_solve_batched_c128",
+                 "ldl_solve_batched_c64", "ldl_solve_batched_c128"):
+        f = getattr(L, name)
+        f.restype = I
+        f.argtypes = solve_args
+    L.hpdinv_solve_kernel_name.restype = ctypes.c_char_p
+    L.hpdinv_solve_kernel_name.argtypes = [I, I, I]
     L.hpdinv_host_workspace_bytes.restype = ctypes.c_size_t
     L.hpdinv_host_workspace_bytes.argtypes = [I, I, I64]
     L.hpdinv_inv_host.restype = I
@@ -46,6 +54,8 @@ def lib() -> ctypes.CDLL:
 EXPORTS = (
     "chol_inv_batched_c64", "chol_inv_batched_c128",
     "ldl_inv_batched_c64", "ldl_inv_batched_c128",
+    "chol_solve_batched_c64", "chol_solve_batched_c128",
+    "ldl_solve_batched_c64", "ldl_solve_batched_c128", "hpdinv_solve_kernel_name",
     "hpdinv_host_workspace_bytes", "hpdinv_inv_host",
     "hpdinv_kernel_name", "hpdinv_version",
 )

@@ -104,9 +104,61 @@ int run(int dtype, bool ldl, const LaunchArgs& c) {
     return rc;
 }
 
+// vectors: interleaved (sm = 1, se >= batch) or contiguous (se = 1, sm >= n)
+bool vec_ok(int64_t batch, int n, int64_t sm, int64_t se) {
+    if (sm < 1 || se < 1) return false;
+    if (n == 1) return true;
+    return (sm == 1 && se >= batch) || (se == 1 && sm >= n);
+}
+
+int run_solve(int dtype, bool ldl, const SolveArgs& c) {
+    const size_t eb = dtype == 0 ? 8 : 16;
+    if (c.batch < 0) return -1;
+    if (c.n < 1 || c.n > HPDINV_MAX_N) return -2;
+    if (c.batch == 0) return 0;
+    if (!c.A || reinterpret_cast<uintptr_t>(c.A) % eb) return -3;
+    if (classify(c.batch, c.n, c.sAm, c.sAe) == kInvalid) return -4;
+    if (!c.Y || reinterpret_cast<uintptr_t>(c.Y) % eb) return -6;
+    if (!vec_ok(c.batch, c.n, c.sYm, c.sYe)) return -7;
+    if (!c.X || reinterpret_cast<uintptr_t>(c.X) % eb) return -9;
+    if (!vec_ok(c.batch, c.n, c.sXm, c.sXe)) return -10;
+    if (!c.info || reinterpret_cast<uintptr_t>(c.info) % 4) return -12;
+    return launch_solve(dtype, ldl, c);
+}
+
 }  // namespace
 
 extern "C" {
+
+int chol_solve_batched_c64(int64_t batch, int n, const cuFloatComplex* A, int64_t sAm, int64_t sAe,
+                           const cuFloatComplex* Y, int64_t sYm, int64_t sYe,
+                           cuFloatComplex* Xv, int64_t sXm, int64_t sXe, int32_t* info, cudaStream_t stream) {
+    return run_solve(0, false, SolveArgs{batch, n, A, sAm, sAe, Y, sYm, sYe, Xv, sXm, sXe, info, stream});
+}
+
+int chol_solve_batched_c128(int64_t batch, int n, const cuDoubleComplex* A, int64_t sAm, int64_t sAe,
+                            const cuDoubleComplex* Y, int64_t sYm, int64_t sYe,
+                            cuDoubleComplex* Xv, int64_t sXm, int64_t sXe, int32_t* info, cudaStream_t stream) {
+    return run_solve(1, false, SolveArgs{batch, n, A, sAm, sAe, Y, sYm, sYe, Xv, sXm, sXe, info, stream});
+}
+
+int ldl_solve_batched_c64(int64_t batch, int n, const cuFloatComplex* A, int64_t sAm, int64_t sAe,
+                          const cuFloatComplex* Y, int64_t sYm, int64_t sYe,
+                          cuFloatComplex* Xv, int64_t sXm, int64_t sXe, int32_t* info, cudaStream_t stream) {
+    return run_solve(0, true, SolveArgs{batch, n, A, sAm, sAe, Y, sYm, sYe, Xv, sXm, sXe, info, stream});
+}
+
+int ldl_solve_batched_c128(int64_t batch, int n, const cuDoubleComplex* A, int64_t sAm, int64_t sAe,
+                           const cuDoubleComplex* Y, int64_t sYm, int64_t sYe,
+                           cuDoubleComplex* Xv, int64_t sXm, int64_t sXe, int32_t* info, cudaStream_t stream) {
+    return run_solve(1, true, SolveArgs{batch, n, A, sAm, sAe, Y, sYm, sYe, Xv, sXm, sXe, info, stream});
+}
+
+const char* hpdinv_solve_kernel_name(int method, int dtype, int n) {
+    if (n < 1 || n > HPDINV_MAX_N || dtype < 0 || dtype > 1) return nullptr;
+    return solve_kernel_name(dtype, method != 0, n);
+}
+
 
 int chol_inv_batched_c64(int64_t batch, int n, const cuFloatComplex* A, int64_t sAm, int64_t sAe,
                          cuFloatComplex* X, int64_t sXm, int64_t sXe, int32_t* info,

@@ -18,6 +18,20 @@ struct LaunchArgs {
     cudaStream_t stream;
 };
 
+// Batched solve A_b x_b = y_b: vectors at base[b*s?m + i*s?e].
+struct SolveArgs {
+    int64_t batch;
+    int n;
+    const void* A;
+    int64_t sAm, sAe;
+    const void* Y;
+    int64_t sYm, sYe;
+    void* X;
+    int64_t sXm, sXe;
+    int32_t* info;
+    cudaStream_t stream;
+};
+
 constexpr int kNoKernel = -1000;   // launcher has no instantiation for this n
 
 // Each returns 0 / cudaError_t of the launch, or kNoKernel.
@@ -26,6 +40,8 @@ int launch_lane(int dtype, bool ldl, const LaunchArgs& a);      // k_lane_c64.cu
 int launch_generic(int dtype, bool ldl, const LaunchArgs& a);   // k_generic.cu
 int launch_grp(int dtype, bool ldl, const LaunchArgs& a);       // k_grp.cu (interleaved, c64 9..16)
 int launch_blk(int dtype, bool ldl, const LaunchArgs& a);       // k_blk.cu (n = 32, 64)
+int launch_solve(int dtype, bool ldl, const SolveArgs& a);      // k_solve.cu (any n <= 64)
+const char* solve_kernel_name(int dtype, bool ldl, int n);
 
 // Largest n of each family per dtype (0 = c64, 1 = c128).
 constexpr int reg_max_n(int dtype) { return dtype == 0 ? 8 : 6; }

@@ -30,6 +30,20 @@ struct BlkShape {
     static constexpr int PR = NB / RT;                // row groups of a GEMM tile grid
     static constexpr int Q = NT / PR;                 // column groups
     static constexpr int CT = (N - NB + Q - 1) / Q;   // max columns per thread (panel width <= n - NB)
+    // lookahead (NT >= 64): one warp runs the serial diagonal-block phases, NT - 32 threads the
+    // GEMM of the rest: QR column groups; CTD columns per lane of the diagonal block's F1;
+    // CTR (F1 rest, width <= n - 2 NB) and CTL (I1 lookahead, width <= n - NB, a power of two
+    // dividing NB) columns per thread
+#ifdef HPDINV_BLK_NOLA
+    static constexpr bool LA = false;
+#else
+    static constexpr bool LA = NT >= 64;
+#endif
+    static constexpr int QR = NT >= 64 ? (NT - 32) / PR : 1;
+    static constexpr int CTD = (NB + (32 / PR) - 1) / (32 / PR);
+    static constexpr int CTR = (N - 2 * NB + QR - 1) / QR > 0 ? (N - 2 * NB + QR - 1) / QR : 1;
+    static constexpr int CTL0 = (N - NB + QR - 1) / QR;
+    static constexpr int CTL = CTL0 <= 1 ? 1 : CTL0 <= 2 ? 2 : CTL0 <= 4 ? 4 : 8;
     static constexpr size_t w_bytes = size_t(N) * LDW * sizeof(cplx<T>);
     static constexpr size_t v_off = ((w_bytes + 15) / 16) * 16;                 // V (NB x NB)
     static constexpr size_t s_off = v_off + size_t(NB) * NB * sizeof(cplx<T>);  // 1/r_kk, d_k
@@ -69,12 +83,13 @@ template <typename T> __device__ __forceinline__ cplx<T> shfl_c(cplx<T> v, int s
 // fp64 subtracts term by term in k order (as written in eqs. 3-4); fp32 accumulates the sum with
 // packed FFMA2 (split accumulator) and subtracts it once.
 template <typename T, int N, int LDW, int RT, int CTT>
-__device__ __forceinline__ void f1(cplx<T>* W, int k0, int p, int q) {
+__device__ __forceinline__ void f1(cplx<T>* W, int k0, int p, int q, int c0 = -1, int cend = N) {
     using V = cplx<T>;
-    if (k0 + q * CTT >= N) return;
+    if (c0 < 0) c0 = k0;
+    if (c0 + q * CTT >= cend) return;
     int jc[CTT];
 #pragma unroll
-    for (int c = 0; c < CTT; c++) { const int j = k0 + q * CTT + c; jc[c] = j < N ? j : N - 1; }
+    for (int c = 0; c < CTT; c++) { const int j = c0 + q * CTT + c; jc[c] = j < cend ? j : cend - 1; }
     const int i0 = k0 + RT * p;
     if constexpr (sizeof(T) == 4) {
         SAcc<T> acc[RT][CTT];
@@ -96,7 +111,7 @@ __device__ __forceinline__ void f1(cplx<T>* W, int k0, int p, int q) {
         }
 #pragma unroll
         for (int c = 0; c < CTT; c++) {
-            if (k0 + q * CTT + c < N) {
+            if (c0 + q * CTT + c < cend) {
 #pragma unroll
                 for (int r = 0; r < RT; r++) {
                     const V sv = sval_conjr(acc[r][c]);          // sum conj(u_ki) r_kj
@@ -125,7 +140,7 @@ __device__ __forceinline__ void f1(cplx<T>* W, int k0, int p, int q) {
         }
 #pragma unroll
         for (int c = 0; c < CTT; c++)
-            if (k0 + q * CTT + c < N) {
+            if (c0 + q * CTT + c < cend) {
 #pragma unroll
                 for (int r = 0; r < RT; r++) W[(i0 + r) * LDW + jc[c]] = acc[r][c];
             }
@@ -136,12 +151,16 @@ __device__ __forceinline__ void f1(cplx<T>* W, int k0, int p, int q) {
 //   W[k][j] = C_kj = sum_{m=t0}^{n-1} r_km x~_mj   (r_km = W[m][k] lower, x~_mj = W[m][j] full X_TT)
 // (it reads rows T only and writes rows K)
 template <typename T, int N, int LDW, int RT, int CTT>
-__device__ __forceinline__ void i1(cplx<T>* W, int k0, int t0, int p, int q) {
+__device__ __forceinline__ void i1(cplx<T>* W, int k0, int t0, int p, int q, int c0 = -1, int mlo = -1) {
     using V = cplx<T>;
-    if (t0 + q * CTT >= N) return;
+    if (c0 < 0) c0 = t0;
+    if (c0 + q * CTT >= N) return;
+    // inner range: m in [mlo, N) (default T); the lookahead passes columns of the block just
+    // inverted with m in T only (their m in K terms wait for X_KK)
+    if (mlo < 0) mlo = t0;
     int jc[CTT];
 #pragma unroll
-    for (int c = 0; c < CTT; c++) { const int j = t0 + q * CTT + c; jc[c] = j < N ? j : N - 1; }
+    for (int c = 0; c < CTT; c++) { const int j = c0 + q * CTT + c; jc[c] = j < N ? j : N - 1; }
     const int kr = k0 + RT * p;
     V cv[RT][CTT];
     if constexpr (sizeof(T) == 4) {
@@ -151,7 +170,7 @@ __device__ __forceinline__ void i1(cplx<T>* W, int k0, int t0, int p, int q) {
 #pragma unroll
             for (int c = 0; c < CTT; c++) sacc_zero(acc[r][c]);
 #pragma unroll 2
-        for (int m = t0; m < N; m++) {
+        for (int m = mlo; m < N; m++) {
             V rk[RT];
 #pragma unroll
             for (int r = 0; r < RT; r++) rk[r] = W[m * LDW + kr + r];
@@ -172,7 +191,7 @@ __device__ __forceinline__ void i1(cplx<T>* W, int k0, int t0, int p, int q) {
 #pragma unroll
             for (int c = 0; c < CTT; c++) cv[r][c] = czero<T>();
 #pragma unroll 2
-        for (int m = t0; m < N; m++) {
+        for (int m = mlo; m < N; m++) {
             V rk[RT];
 #pragma unroll
             for (int r = 0; r < RT; r++) rk[r] = W[m * LDW + kr + r];
@@ -186,7 +205,7 @@ __device__ __forceinline__ void i1(cplx<T>* W, int k0, int t0, int p, int q) {
     }
 #pragma unroll
     for (int c = 0; c < CTT; c++)
-        if (t0 + q * CTT + c < N) {
+        if (c0 + q * CTT + c < N) {
 #pragma unroll
             for (int r = 0; r < RT; r++) W[(kr + r) * LDW + jc[c]] = cv[r][c];
         }
@@ -238,13 +257,27 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
     for (int k0 = 0; k0 < N; k0 += NB) {
         BLK_PHASE(0);
         // ---- F1: P = A_K,[k0,n) - U_{<k0,K}^H R_{<k0,[k0,n)}  (k ascending, as in eqs. 3-4)
-        if (k0 > 0) {
-            const int ct = (N - k0 + Q - 1) / Q;     // columns per thread for this panel width
-            if (ct == 1) blk::f1<T, N, LDW, RT, 1>(W, k0, p, q);
-            else if (ct == 2) blk::f1<T, N, LDW, RT, (CT >= 2 ? 2 : 1)>(W, k0, p, q);
-            else blk::f1<T, N, LDW, RT, CT>(W, k0, p, q);
+        if constexpr (Sh::LA) {
+            // lookahead: the serial warp computes the diagonal block of P and factors it (F2a)
+            // while the other warps compute the rest of the panel (nothing below depends on it)
+            if (warp == swarp) {
+                if (k0 > 0) blk::f1<T, N, LDW, RT, Sh::CTD>(W, k0, lane % PR, lane / PR, k0, k0 + NB);
+                __syncwarp();
+            } else if (k0 > 0 && k0 + NB < N) {
+                const int rt = tid - (warp > swarp ? 32 : 0), pr = rt % PR, qr = rt / PR;
+                const int ct = (N - k0 - NB + Sh::QR - 1) / Sh::QR;
+                if (ct == 1) blk::f1<T, N, LDW, RT, 1>(W, k0, pr, qr, k0 + NB, N);
+                else blk::f1<T, N, LDW, RT, Sh::CTR>(W, k0, pr, qr, k0 + NB, N);
+            }
+        } else {
+            if (k0 > 0) {
+                const int ct = (N - k0 + Q - 1) / Q;     // columns per thread for this panel width
+                if (ct == 1) blk::f1<T, N, LDW, RT, 1>(W, k0, p, q);
+                else if (ct == 2) blk::f1<T, N, LDW, RT, (CT >= 2 ? 2 : 1)>(W, k0, p, q);
+                else blk::f1<T, N, LDW, RT, CT>(W, k0, p, q);
+            }
+            __syncthreads();
         }
-        __syncthreads();
         BLK_PHASE(1);
         // ---- F2a: diagonal block, warp swarp, lane l owns column k0 + l; row i of U is broadcast
         //      through shared memory, the pivot by one shuffle
@@ -254,15 +287,20 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
 #pragma unroll
             for (int m = 0; m < NB; m++) pc[m] = WE(k0 + m, k0 + l);
             int bad_first = 0;
+            T tnext = pc[0].x;
 #pragma unroll
             for (int i = 0; i < NB; i++) {
-                const T t = __shfl_sync(0xffffffffu, pc[i].x, i);
+                // the pivot comes from lane i's own update of its diagonal entry in the previous
+                // step (u_{i-1,i} is its own value), bitwise what the shared-memory path gives,
+                // so the serial chain skips the row exchange
+                const T t = __shfl_sync(0xffffffffu, tnext, i);
                 const bool bad = !(t > T(0));
                 if (bad && bad_first == 0) bad_first = k0 + i + 1;
                 const T tt = bad ? T(1) : t;                   // flagged: keep the arithmetic finite
                 const T iv = LDL ? rcp_fast(tt) : rsqrt_fast(tt);
                 const V r = cscale(pc[i], iv);                 // r_{k0+i, k0+l}, l > i
                 const V u = LDL ? cscale(r, tt) : r;           // u = d r (LDL)
+                if (i + 1 < NB) { V d = pc[i + 1]; cfms_conj(d, u, r); tnext = d.x; }
                 if (lane == i) { invs[k0 + i] = iv; if (LDL) dgs[k0 + i] = tt; }
                 if (lane > i && lane < NB) {
                     WE(k0 + i, k0 + lane) = u;                 // U row (upper)
@@ -307,14 +345,18 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
     for (int k0 = N - NB; k0 >= 0; k0 -= NB) {
         const int t0 = k0 + NB;                       // T = [t0, n)
         BLK_PHASE(3);
-        // ---- I1: C = R_KT X_TT into the upper K x T block (R_KT's upper copy is dead)
-        if (t0 < N) {
-            const int ct = (N - t0 + Q - 1) / Q;
-            if (ct == 1) blk::i1<T, N, LDW, RT, 1>(W, k0, t0, p, q);
-            else if (ct == 2) blk::i1<T, N, LDW, RT, (CT >= 2 ? 2 : 1)>(W, k0, t0, p, q);
-            else blk::i1<T, N, LDW, RT, CT>(W, k0, t0, p, q);
+        // ---- I1: C = R_KT X_TT into the upper K x T block (R_KT's upper copy is dead).  With
+        //      the lookahead (NT >= 64) it was computed during the previous panel's I4, all but
+        //      the terms m in K_prev = [t0, t0+NB) of the columns j in K_prev (added in I2)
+        if constexpr (!Sh::LA) {
+            if (t0 < N) {
+                const int ct = (N - t0 + Q - 1) / Q;
+                if (ct == 1) blk::i1<T, N, LDW, RT, 1>(W, k0, t0, p, q);
+                else if (ct == 2) blk::i1<T, N, LDW, RT, (CT >= 2 ? 2 : 1)>(W, k0, t0, p, q);
+                else blk::i1<T, N, LDW, RT, CT>(W, k0, t0, p, q);
+            }
+            __syncthreads();
         }
-        __syncthreads();
         BLK_PHASE(4);
         // ---- I2: rows K of the columns j in T, bottom-up (x_mj, m in K, stays in registers)
         V xk[NB];
@@ -371,6 +413,19 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
                 for (int kk = 0; kk < NB; kk++) WE(j, k0 + kk) = conjz(xk[kk]);
             }
         }
+        if constexpr (Sh::LA) {
+            __syncthreads();              // the lookahead below reads the mirror
+            // lookahead I1 of the next panel K' = [k0-NB, k0), T' = [k0, n), by the warps that
+            // do not run I4: columns j in T with m in T', columns j in K with m in T only
+            if (warp != swarp && k0 > 0) {
+                const int rt = tid - (warp > swarp ? 32 : 0), pr = rt % PR, qr = rt / PR;
+                const int ct = (N - k0 + Sh::QR - 1) / Sh::QR;
+                // CC columns per thread divides NB: each thread has one m range
+                if (ct <= 1) blk::i1<T, N, LDW, RT, 1>(W, k0 - NB, k0, pr, qr, k0, k0 + qr < t0 ? t0 : k0);
+                else if (ct <= 2) blk::i1<T, N, LDW, RT, 2>(W, k0 - NB, k0, pr, qr, k0, k0 + 2 * qr < t0 ? t0 : k0);
+                else blk::i1<T, N, LDW, RT, Sh::CTL>(W, k0 - NB, k0, pr, qr, k0, k0 + Sh::CTL * qr < t0 ? t0 : k0);
+            }
+        }
         BLK_PHASE(6);
         // ---- I4: the diagonal block, warp swarp, lane l owns column k0 + l (full column in registers);
         //      row k of X goes to W at once (it overwrites the dead upper U row k) and the owner
@@ -414,6 +469,20 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
             }
         }
         __syncthreads();
+        if constexpr (Sh::LA) {
+            // lookahead: the terms m in K of the next panel's C_kj for the columns j in K (they
+            // needed X_KK); k in K' = [k0-NB, k0)
+            if (k0 > 0) {
+                for (int o = tid; o < NB * NB; o += NT) {
+                    const int k = k0 - NB + o / NB, j = k0 + o % NB;
+                    V sv = WE(k, j);
+#pragma unroll
+                    for (int m = 0; m < NB; m++) cfma(sv, WE(k0 + m, k), WE(k0 + m, j));
+                    WE(k, j) = sv;
+                }
+            }
+            __syncthreads();
+        }
     }
     }
 

@@ -14,30 +14,11 @@ namespace hpdinv {
 
 constexpr int kRegThreads = 128;
 
+// S2 / S2': factorisation of the packed upper triangle r[] in place (eqs. 3-4 / 10-11; sums
+// in k ascending as written); LDL keeps d_i on the diagonal.  inv[i] = 1/r_ii (1/d_i).
+// Returns info: the first 1-based i with !(t_i > 0), else 0.
 template <typename T, int N, bool LDL>
-__global__ void __launch_bounds__(kRegThreads)
-k_reg(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
-      cplx<T>* X, int64_t sXm, int64_t sXe, int32_t* __restrict__ info)
-{
-    constexpr int NU = N * (N + 1) / 2;
-    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (b >= batch) return;
-
-    cplx<T> r[NU];
-    T inv[N];
-    const cplx<T>* Ab = A + b * sAm;
-#pragma unroll
-    for (int i = 0; i < N; i++)
-#pragma unroll
-        for (int j = 0; j < N; j++) {
-            if (j >= i) {
-                cplx<T> v = __ldg(Ab + int64_t(i * N + j) * sAe);
-                if (i == j) v.y = T(0);
-                r[upk(N, i, j)] = v;
-            }
-        }
-
-    // ---- S2: factorisation (right-to-left sums in k ascending, as written in eqs. 3-4)
+__device__ __forceinline__ int reg_factor(cplx<T> (&r)[N * (N + 1) / 2], T (&inv)[N]) {
     int inf = 0;
 #pragma unroll
     for (int i = 0; i < N; i++) {
@@ -79,6 +60,35 @@ k_reg(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
             r[upk(N, i, j)] = cscale(s, iv);
         }
     }
+
+    return inf;
+}
+
+template <typename T, int N, bool LDL>
+__global__ void __launch_bounds__(kRegThreads)
+k_reg(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
+      cplx<T>* X, int64_t sXm, int64_t sXe, int32_t* __restrict__ info)
+{
+    constexpr int NU = N * (N + 1) / 2;
+    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= batch) return;
+
+    cplx<T> r[NU];
+    T inv[N];
+    const cplx<T>* Ab = A + b * sAm;
+#pragma unroll
+    for (int i = 0; i < N; i++)
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+            if (j >= i) {
+                cplx<T> v = __ldg(Ab + int64_t(i * N + j) * sAe);
+                if (i == j) v.y = T(0);
+                r[upk(N, i, j)] = v;
+            }
+        }
+
+    // ---- S2: factorisation
+    const int inf = reg_factor<T, N, LDL>(r, inv);
 
     // ---- S3/S4: proposed inversion, rows k = N-1..0, in place over R's upper triangle
 #pragma unroll

@@ -37,6 +37,7 @@ class Config:
     divisor: float = 1.0   # A = B B^H / divisor + delta I
     delta: float = 0.0
     desc: str = ""
+    task: str = "inv"      # "inv" (the hot path) | "solve" (A x = y)
 
     @property
     def elem_bytes(self) -> int:
@@ -54,6 +55,11 @@ CONFIGS = {
               "2^18 c128 HPD 64x64, A = Q diag(lam) Q^H, lam log-uniform [1,1e3], one matrix per CTA"),
     5: Config(5, 32, torch.complex64, 1 << 20, "ldl", "aos", "bbh", 32.0, 0.05,
               "2^20 c64 HPD 32x32, A = BB^H/32 + 0.05I, LDL R*DR + proposed"),
+    # SURVEY §8(f) f1 (next row, not a BASELINE.json config): the cfg2 matrices, one
+    # right-hand side y ~ CN(0, I) each, solved by eqs. (5)-(7)
+    6: Config(6, 8, torch.complex64, 1 << 20, "chol", "soa", "bbh", 8.0, 0.1,
+              "2^20 c64 HPD 8x8 systems A x = y (cfg2 matrices, y ~ CN(0,I)), Cholesky solve eqs. 5-7, "
+              "interleaved", task="solve"),
 }
 
 
@@ -107,6 +113,41 @@ def generate(cfg: Config, start: int = 0, count: Optional[int] = None, device="c
         out[pos - start:pos - start + take] = chunk[pos - c0:pos - c0 + take]
         pos += take
     return out
+
+
+def generate_rhs(cfg: Config, start: int = 0, count: Optional[int] = None, device="cpu",
+                 seed: int = 0) -> torch.Tensor:
+    """Right-hand sides [start, start+count) for config `cfg` (f1 solve): (count, n), entries
+    i.i.d. CN(0,1); chunk-keyed like `generate` (stream id 1000 + config id)."""
+    if count is None:
+        count = cfg.batch - start
+    out = torch.empty(count, cfg.n, dtype=cfg.dtype, device=device)
+    pos = start
+    while pos < start + count:
+        c = pos // CHUNK
+        c0 = c * CHUNK
+        take = min(c0 + CHUNK, start + count) - pos
+        g = torch.Generator(device=device)
+        g.manual_seed(chunk_seed(seed, 1000 + cfg.cid, c))
+        chunk = torch.randn(CHUNK, cfg.n, dtype=cfg.dtype, device=device, generator=g)
+        out[pos - start:pos - start + take] = chunk[pos - c0:pos - c0 + take]
+        pos += take
+    return out
+
+
+def vec_layout(Y: torch.Tensor, layout: str, ld: Optional[int] = None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Copy contiguous (batch, n) vectors into `layout` ("aos": contiguous; "soa": element i of
+    system b at planes[i, b], ld >= batch).  Returns (storage, (batch, n) view)."""
+    batch, n = Y.shape
+    if layout == "aos":
+        buf = Y.contiguous()
+        return buf, buf
+    ld = batch if ld is None else ld
+    planes = torch.empty(n, ld, dtype=Y.dtype, device=Y.device)
+    planes[:, :batch] = Y.t()
+    if ld > batch:
+        planes[:, batch:] = float("nan")
+    return planes, torch.as_strided(planes, (batch, n), (1, ld))
 
 
 def soa_view(planes: torch.Tensor, batch: int, n: int) -> torch.Tensor:

@@ -52,6 +52,18 @@ def test_validation_without_gpu(lib):
     assert lib.hpdinv_host_workspace_bytes(0, 8, 1024) >= 2 * 64 * 8 * 1024
     assert lib.hpdinv_inv_host(0, 0, 4, 8, z, 1, 4, z, 1, 4, z, z, 0, 0, z) == -5
     assert b"sm_100a" in lib.hpdinv_version()
+    # batched solve (f1): same conventions, vectors interleaved or contiguous
+    assert lib.chol_solve_batched_c64(0, 8, z, 1, 0, z, 1, 0, z, 1, 0, z, z) == 0
+    assert lib.ldl_solve_batched_c128(-1, 8, z, 1, 8, z, 1, 8, z, 1, 8, z, z) == -1
+    assert lib.chol_solve_batched_c128(4, 65, z, 1, 8, z, 1, 8, z, 1, 8, z, z) == -2
+    assert lib.chol_solve_batched_c64(4, 8, z, 1, 8, z, 1, 8, z, 1, 8, z, z) == -3
+    assert lib.chol_solve_batched_c64(4, 8, fake, 1, 4, z, 1, 4, z, 1, 4, z, z) == -6
+    assert lib.chol_solve_batched_c64(4, 8, fake, 1, 4, fake, 2, 2, z, 1, 4, z, z) == -7
+    assert lib.chol_solve_batched_c64(4, 8, fake, 1, 4, fake, 8, 1, fake, 7, 1, z, z) == -10
+    assert lib.ldl_solve_batched_c64(4, 8, fake, 1, 4, fake, 8, 1, fake, 1, 4, z, z) == -12
+    assert lib.hpdinv_solve_kernel_name(0, 0, 8) == b"k_solve_reg<c64,chol>"
+    assert lib.hpdinv_solve_kernel_name(1, 1, 64) == b"k_solve_gen<c128,ldl>"
+    assert lib.hpdinv_solve_kernel_name(0, 0, 65) is None
 
 
 def test_no_cpu_fallback_in_product_path():
