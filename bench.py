@@ -48,6 +48,9 @@ def parse():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-library", action="store_true", help="skip the vendor-library comparison")
+    p.add_argument("--inv-method", choices=["proposed", "eqsolve", "trimat"], default="proposed",
+                   help="SURVEY 8(f) f3: time one of the paper's existing methods on the GPU instead")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     return p.parse_args()
 
@@ -63,12 +66,16 @@ def algorithmic_bytes(cfg: wl.Config) -> int:
     n, e = cfg.n, cfg.elem_bytes
     if cfg.task == "solve":
         return e * (n * (n + 1) // 2 + 2 * n) + 4
+    if cfg.task == "nonherm":         # read all of D, write D^-1
+        return e * 2 * n * n + 4
     return e * (n * (n + 1) // 2 + n * n) + 4
 
 
 def cmul_per_matrix(n: int, task: str = "inv") -> int:
     if task == "solve":               # factor (n^3-n)/6 + two substitutions n(n-1)/2 each
         return (n ** 3 - n) // 6 + n * (n - 1)
+    if task == "nonherm":             # D D* (upper) + Cholesky + proposed + D* X
+        return n * n * (n + 1) // 2 + (n ** 3 - n) // 2 + n ** 3
     return (n ** 3 - n) // 2          # Table 1 proposed total, exact
 
 
@@ -193,6 +200,18 @@ def run_ours(args, rank, world, local_rank):
 
         def step():
             hp.solve(view, yview, cfg.method, Xv=Xv, info=info)
+    elif cfg.task == "nonherm":
+        X = wl.empty_like_layout(view)
+        kernel = hp.nonherm_kernel_name(cfg.dtype, cfg.n)
+
+        def step():
+            hp.invert_nonhermitian(view, Dinv=X, info=info)
+    elif args.inv_method != "proposed":
+        X = wl.empty_like_layout(view)
+        kernel = hp.method_kernel_name(args.inv_method, cfg.dtype, cfg.n)
+
+        def step():
+            hp.invert_method(view, args.inv_method, X=X, info=info)
     else:
         X = wl.empty_like_layout(view)
         kernel = hp.kernel_name(cfg.method, cfg.dtype, B, cfg.n, (view.stride(0), view.stride(2)))
@@ -241,7 +260,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- end to end through the host-buffer C entry point (H2D + kernel + D2H timed)
     e2e = None
-    if not args.no_e2e and not solve:
+    if not args.no_e2e and cfg.task == "inv" and args.inv_method == "proposed":
         A_host = store.cpu().pin_memory()
         if cfg.layout == "soa":
             vh = wl.soa_view(A_host, B, cfg.n)
@@ -321,14 +340,70 @@ def run_ours(args, rank, world, local_rank):
                                       "bytes": bj_bytes, "note": "BASELINE.json north_star formula"},
         "clocks": clocks, "gpu_launches": steps, "info_nonzero": bad, "e2e": e2e,
     }
-    if solve:
-        out["config"]["task"] = "solve (1 right-hand side per matrix)"
+    if args.inv_method != "proposed":
+        out["config"]["inv_method"] = args.inv_method + " (SURVEY 8(f) f3: the paper's existing method, not the product path)"
         out.pop("roofline_baseline_formula")
+    if cfg.task != "inv":
+        out["config"]["task"] = ("solve (1 right-hand side per matrix)" if solve else
+                                 "non-Hermitian inversion D^-1 = D*(DD*)^-1")
+        out.pop("roofline_baseline_formula", None)
         if e2e is None:
-            out["e2e_note"] = "the solve has no host-buffer entry point yet"
+            out["e2e_note"] = "no host-buffer entry point for this task yet"
+        if cfg.task == "nonherm":
+            out["metric"] = "non-Hermitian matrices inverted/sec (SURVEY 8(f) f2, P:135-141), 1 B200"
+    if rank == 0 and world == 1 and not args.no_library:
+        out["library_baseline"] = library_baseline(cfg, view, yview if solve else None, dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, args, budget_s=args.cpu_seconds, dev=dev)
     return out
+
+
+# ------------------------------------------------------- vendor-library comparison (context)
+def library_baseline(cfg: wl.Config, view, yview, dev, steps: int = 5):
+    """The same workload through PyTorch's batched dense linear algebra on the same GPU
+    (cuSOLVER / cuBLAS / MAGMA batched kernels behind torch.linalg): Cholesky + cholesky_inverse
+    (the potrf + potri route of SURVEY App. A.3, 'trimat') and, for the solve, cholesky_solve.
+    Full Hermitian AoS matrices are formed once outside the timed region.  Context only: it
+    is not our kernel and not the reference arm."""
+    try:
+        B, n = view.shape[0], view.shape[1]
+        Af = view.contiguous()
+        if cfg.task != "nonherm":
+            Af = torch.triu(Af) + torch.triu(Af, 1).conj().transpose(1, 2)
+        if cfg.task == "nonherm":
+            Af = view.contiguous()
+
+            def run():
+                return torch.linalg.inv_ex(Af)[0]
+            what = "torch.linalg.inv_ex (batched LU)"
+        elif yview is not None:
+            y = yview.contiguous().unsqueeze(-1)
+
+            def run():
+                L, _ = torch.linalg.cholesky_ex(Af)
+                return torch.cholesky_solve(y, L)
+            what = "torch.linalg.cholesky_ex + torch.cholesky_solve"
+        else:
+            def run():
+                L, _ = torch.linalg.cholesky_ex(Af)
+                return torch.cholesky_inverse(L)
+            what = "torch.linalg.cholesky_ex + torch.cholesky_inverse"
+        for _ in range(2):
+            run()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            run()
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / steps
+        del Af
+        return {"value": B / (ms / 1e3), "unit": UNIT_SOLVE if yview is not None else UNIT, "ms_per_step": ms,
+                "what": what + " on full Hermitian AoS matrices, same GPU, %d steps" % steps}
+    except Exception as e:  # pragma: no cover - library availability depends on the box
+        torch.cuda.synchronize()
+        return {"unavailable": repr(e)[:200]}
 
 
 # ------------------------------------------------------------------- the oracle arm
@@ -341,6 +416,8 @@ def oracle_sample(cfg: wl.Config, count: int, seed: int, dev):
 
 def oracle_run(cfg: wl.Config, Ah, yh):
     import oracle
+    if cfg.task == "nonherm":
+        return oracle.nonherm_batched(Ah)
     if cfg.task == "solve":
         return oracle.solve_batched(Ah, yh, cfg.method)
     return oracle.inv_batched(Ah, cfg.method)

@@ -134,6 +134,48 @@ int ldl_solve_batched_c128(int64_t batch, int n,
 const char *hpdinv_solve_kernel_name(int method, int dtype, int n);
 
 /* ---------------------------------------------------------------------------------------
+ * The paper's existing inversion methods on the GPU, for measuring the
+ * Table 1 comparison on B200.  All start from the Cholesky factor (eqs. 3-4):
+ *   method 0 / 1: the proposed method (Cholesky / LDL) -- exactly chol_/ldl_inv_batched_*;
+ *   method 2: equation solving, eq. (15), P:103-113 (R* b_i = e_i, then R x_i = b_i);
+ *   method 3: triangular matrix operations, eqs. (16)-(19), P:115-133 (M = R^-1, X = M M*).
+ * dtype 0 = complex64, 1 = complex128.  Arguments 3..12 and the contract (layouts, info, NaN
+ * fill, mirror, stream order, no allocation) are those of chol_inv_batched_*; returns 0, -k for
+ * invalid argument k (1 method, 2 dtype, 3 batch, 4 n, 5 A, ...), or a cudaError_t.  Methods
+ * 2 and 3: one matrix per thread in registers for n <= 8 (c64) / n <= 6 (c128), otherwise one
+ * matrix per CTA (correctness path). */
+int hpdinv_inv_batched_method(int method, int dtype, int64_t batch, int n,
+                              const void *A, int64_t strideA_mat, int64_t strideA_elem,
+                              void *X, int64_t strideX_mat, int64_t strideX_elem,
+                              int32_t *info, cudaStream_t stream);
+
+/* Kernel a method-2/3 call would launch (static string; NULL for methods 0/1 or bad args). */
+const char *hpdinv_method_kernel_name(int method, int dtype, int n);
+
+/* ---------------------------------------------------------------------------------------
+ * Non-Hermitian inversion through the HPD path: for an
+ * arbitrary nonsingular D, A = D D* is HPD; X = A^-1 by Cholesky (eqs. 3-4) + the proposed
+ * inversion (eqs. 20-24); D^-1 = D* X.  Fused in one launch (D read, D^-1 written).
+ *   D, Dinv: element (i,j) of matrix b at base[b*stride_mat + (i*n+j)*stride_elem] (ALL n^2
+ *     entries of D are read); layouts and argument numbering as chol_inv_batched_*; Dinv may
+ *     not overlap D.
+ *   info[b]: the Cholesky info of A_b = D_b D_b* (0 <=> numerically nonsingular); Dinv_b is
+ *     NaN when info[b] != 0.
+ * Kernels: one matrix per thread in registers for n <= 8 (c64) / n <= 6 (c128), otherwise one
+ * matrix per CTA. */
+int nonherm_inv_batched_c64(int64_t batch, int n,
+                            const cuFloatComplex *D, int64_t strideD_mat, int64_t strideD_elem,
+                            cuFloatComplex *Dinv, int64_t strideX_mat, int64_t strideX_elem,
+                            int32_t *info, cudaStream_t stream);
+int nonherm_inv_batched_c128(int64_t batch, int n,
+                             const cuDoubleComplex *D, int64_t strideD_mat, int64_t strideD_elem,
+                             cuDoubleComplex *Dinv, int64_t strideX_mat, int64_t strideX_elem,
+                             int32_t *info, cudaStream_t stream);
+
+/* Kernel the non-Hermitian entry point launches (static string; NULL if invalid). */
+const char *hpdinv_nonherm_kernel_name(int dtype, int n);
+
+/* ---------------------------------------------------------------------------------------
  * Host-buffer entry point (end-to-end use from host memory).
  *
  * hpdinv_inv_host runs the same hot path on matrices that live in HOST memory (pinned

@@ -76,6 +76,7 @@ def lib() -> ctypes.CDLL:
             "oracle_nonhermitian_inv": (I, [I, P, P]),
             "oracle_inv_batched": (I, [I64, I, P, I64, I64, P, I64, I64, P, I, I]),
             "oracle_solve_batched": (I, [I64, I, P, I64, I64, P, P, P, I, I]),
+            "oracle_nonherm_batched": (I, [I64, I, P, P, P, I]),
             "oracle_max_threads": (I, []),
         }
         for name, (res, args) in sig.items():
@@ -238,6 +239,18 @@ def solve_batched(A: np.ndarray, y: np.ndarray, method: str = "chol", nthreads: 
     if rc != 0:
         raise ValueError("oracle_solve_batched rejected its arguments (rc=%d)" % rc)
     return x, info
+
+
+def nonherm_batched(D: np.ndarray, nthreads: int = 0):
+    """Batched D^-1 = D* (D D*)^-1.  D: (batch, n, n)."""
+    D = np.ascontiguousarray(_c128(D))
+    batch, n = D.shape[0], D.shape[1]
+    Dinv = np.empty_like(D)
+    info = np.zeros(batch, np.int32)
+    rc = lib().oracle_nonherm_batched(batch, n, _ptr(D), _ptr(Dinv), _ptr(info), int(nthreads))
+    if rc != 0:
+        raise ValueError("oracle_nonherm_batched rejected its arguments (rc=%d)" % rc)
+    return Dinv, info
 
 
 def max_threads() -> int:

@@ -411,6 +411,23 @@ int oracle_solve_batched(int64_t batch, int n, const double complex *A, int64_t 
     return 0;
 }
 
+/* Batched non-Hermitian inversion, one oracle_nonhermitian_inv per matrix.
+ * D: contiguous batch x n x n; Dinv likewise; OpenMP across matrices only. */
+int oracle_nonherm_batched(int64_t batch, int n, const double complex *D, double complex *Dinv,
+                           int32_t *info, int nthreads)
+{
+    if (batch < 0 || n < 1) return -1;
+    if (batch == 0) return 0;
+    size_t nn = (size_t)n * (size_t)n;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel for schedule(static) num_threads(nthreads)
+#endif
+    for (int64_t b = 0; b < batch; b++)
+        info[b] = oracle_nonhermitian_inv(n, D + (size_t)b * nn, Dinv + (size_t)b * nn);
+    return 0;
+}
+
 int oracle_max_threads(void)
 {
 #ifdef _OPENMP

@@ -103,6 +103,11 @@ int oracle_solve_batched(int64_t batch, int n, const double complex *A, int64_t 
                          int64_t sA_elem, const double complex *y, double complex *x,
                          int32_t *info, int method, int nthreads);
 
+/* Batched non-Hermitian inversion: contiguous batch x n x n D and Dinv;
+ * info[b] = the Cholesky info of D_b D_b*. */
+int oracle_nonherm_batched(int64_t batch, int n, const double complex *D, double complex *Dinv,
+                           int32_t *info, int nthreads);
+
 /* Number of OpenMP threads a parallel region would use (for the reported core count). */
 int oracle_max_threads(void);
 

@@ -20,7 +20,9 @@ from ._lib import EXPORTS, HpdinvError, lib  # noqa: F401
 __all__ = [
     "chol_inv_batched_c64", "chol_inv_batched_c128", "ldl_inv_batched_c64",
     "ldl_inv_batched_c128", "chol_solve_batched_c64", "chol_solve_batched_c128",
-    "ldl_solve_batched_c64", "ldl_solve_batched_c128", "solve", "solve_kernel_name", "invert", "invert_host", "host_workspace_bytes", "kernel_name", "version", "HpdinvError",
+    "ldl_solve_batched_c64", "ldl_solve_batched_c128", "solve", "solve_kernel_name", "invert",
+    "invert_method", "method_kernel_name", "nonherm_inv_batched_c64", "nonherm_inv_batched_c128",
+    "invert_nonhermitian", "nonherm_kernel_name", "invert_host", "host_workspace_bytes", "kernel_name", "version", "HpdinvError",
 ]
 
 
@@ -167,6 +169,58 @@ def solve(A, Y, method: str = "chol", Xv=None, info=None, stream=None):
 
 def solve_kernel_name(method: str, dtype: torch.dtype, n: int):
     r = lib().hpdinv_solve_kernel_name({"chol": 0, "ldl": 1}[method], {torch.complex64: 0, torch.complex128: 1}[dtype], n)
+    return r.decode() if r else None
+
+
+def nonherm_inv_batched_c64(D, Dinv=None, info=None, stream=None):
+    """D^-1 = D* (D D*)^-1 via Cholesky + the proposed inversion, complex64."""
+    return _call("nonherm_inv_batched_c64", torch.complex64, D, Dinv, info, stream)
+
+
+def nonherm_inv_batched_c128(D, Dinv=None, info=None, stream=None):
+    """D^-1 = D* (D D*)^-1 via Cholesky + the proposed inversion, complex128."""
+    return _call("nonherm_inv_batched_c128", torch.complex128, D, Dinv, info, stream)
+
+
+def invert_nonhermitian(D, Dinv=None, info=None, stream=None):
+    """Batched inverse of arbitrary (non-Hermitian) matrices."""
+    f = nonherm_inv_batched_c64 if D.dtype == torch.complex64 else nonherm_inv_batched_c128
+    return f(D, Dinv, info, stream)
+
+
+def nonherm_kernel_name(dtype: torch.dtype, n: int):
+    r = lib().hpdinv_nonherm_kernel_name({torch.complex64: 0, torch.complex128: 1}[dtype], n)
+    return r.decode() if r else None
+
+
+METHOD_IDS = {"chol": 0, "ldl": 1, "eqsolve": 2, "trimat": 3}
+
+
+def invert_method(A, method: str, X=None, info=None, stream=None):
+    """hpdinv_inv_batched_method: the paper's existing methods on the GPU --
+    "eqsolve" (eq. 15) and "trimat" (eqs. 16-19) -- or the proposed "chol" / "ldl"."""
+    dtype = {torch.complex64: 0, torch.complex128: 1}[A.dtype]
+    if not A.is_cuda:
+        raise ValueError("invert_method: A must be a CUDA tensor (no CPU path exists)")
+    batch, n = A.shape[0], A.shape[1]
+    sAm, sAe = _strides(A)
+    if X is None:
+        X = torch.empty_strided(A.shape, A.stride(), dtype=A.dtype, device=A.device)
+    sXm, sXe = _strides(X)
+    if info is None:
+        info = torch.empty(batch, dtype=torch.int32, device=A.device)
+    rc = lib().hpdinv_inv_batched_method(METHOD_IDS[method], dtype, batch, n, ctypes.c_void_p(A.data_ptr()),
+                                         sAm, sAe, ctypes.c_void_p(X.data_ptr()), sXm, sXe,
+                                         ctypes.c_void_p(info.data_ptr()), ctypes.c_void_p(_stream_handle(stream)))
+    if rc < 0:
+        raise ValueError("hpdinv_inv_batched_method rejected argument %d" % (-rc))
+    if rc > 0:
+        raise HpdinvError("hpdinv_inv_batched_method: CUDA error %d at launch" % rc)
+    return X, info
+
+
+def method_kernel_name(method: str, dtype: torch.dtype, n: int):
+    r = lib().hpdinv_method_kernel_name(METHOD_IDS[method], {torch.complex64: 0, torch.complex128: 1}[dtype], n)
     return r.decode() if r else None
 
 

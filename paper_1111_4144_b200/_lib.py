@@ -35,6 +35,16 @@ def lib() -> ctypes.CDLL:
         f = getattr(L, name)
         f.restype = I
         f.argtypes = solve_args
+    for name in ("nonherm_inv_batched_c64", "nonherm_inv_batched_c128"):
+        f = getattr(L, name)
+        f.restype = I
+        f.argtypes = inv_args
+    L.hpdinv_nonherm_kernel_name.restype = ctypes.c_char_p
+    L.hpdinv_nonherm_kernel_name.argtypes = [I, I]
+    L.hpdinv_inv_batched_method.restype = I
+    L.hpdinv_inv_batched_method.argtypes = [I, I] + inv_args
+    L.hpdinv_method_kernel_name.restype = ctypes.c_char_p
+    L.hpdinv_method_kernel_name.argtypes = [I, I, I]
     L.hpdinv_solve_kernel_name.restype = ctypes.c_char_p
     L.hpdinv_solve_kernel_name.argtypes = [I, I, I]
     L.hpdinv_host_workspace_bytes.restype = ctypes.c_size_t
@@ -56,6 +66,8 @@ EXPORTS = (
     "ldl_inv_batched_c64", "ldl_inv_batched_c128",
     "chol_solve_batched_c64", "chol_solve_batched_c128",
     "ldl_solve_batched_c64", "ldl_solve_batched_c128", "hpdinv_solve_kernel_name",
+    "hpdinv_inv_batched_method", "hpdinv_method_kernel_name",
+    "nonherm_inv_batched_c64", "nonherm_inv_batched_c128", "hpdinv_nonherm_kernel_name",
     "hpdinv_host_workspace_bytes", "hpdinv_inv_host",
     "hpdinv_kernel_name", "hpdinv_version",
 )

@@ -154,6 +154,46 @@ int ldl_solve_batched_c128(int64_t batch, int n, const cuDoubleComplex* A, int64
     return run_solve(1, true, SolveArgs{batch, n, A, sAm, sAe, Y, sYm, sYe, Xv, sXm, sXe, info, stream});
 }
 
+int hpdinv_inv_batched_method(int method, int dtype, int64_t batch, int n, const void* A, int64_t sAm,
+                              int64_t sAe, void* X, int64_t sXm, int64_t sXe, int32_t* info,
+                              cudaStream_t stream) {
+    if (dtype < 0 || dtype > 1) return -2;
+    if (method < 0 || method > 3) return -1;
+    const LaunchArgs c{batch, n, A, sAm, sAe, X, sXm, sXe, info, stream};
+    int rc;
+    if (method <= 1) {
+        rc = run(dtype, method == 1, c);
+    } else {
+        const int v = validate(c, dtype == 0 ? 8 : 16);
+        rc = v <= 0 ? v : launch_base(method, dtype, c);
+    }
+    return (rc < 0 && rc > kNoKernel) ? rc - 2 : rc;   // argument k of the 10-argument form is k+2 here
+}
+
+int nonherm_inv_batched_c64(int64_t batch, int n, const cuFloatComplex* D, int64_t sDm, int64_t sDe,
+                            cuFloatComplex* Dinv, int64_t sXm, int64_t sXe, int32_t* info, cudaStream_t stream) {
+    const LaunchArgs c{batch, n, D, sDm, sDe, Dinv, sXm, sXe, info, stream};
+    const int v = validate(c, 8);
+    return v <= 0 ? v : launch_nh(0, c);
+}
+
+int nonherm_inv_batched_c128(int64_t batch, int n, const cuDoubleComplex* D, int64_t sDm, int64_t sDe,
+                             cuDoubleComplex* Dinv, int64_t sXm, int64_t sXe, int32_t* info, cudaStream_t stream) {
+    const LaunchArgs c{batch, n, D, sDm, sDe, Dinv, sXm, sXe, info, stream};
+    const int v = validate(c, 16);
+    return v <= 0 ? v : launch_nh(1, c);
+}
+
+const char* hpdinv_nonherm_kernel_name(int dtype, int n) {
+    if (n < 1 || n > HPDINV_MAX_N || dtype < 0 || dtype > 1) return nullptr;
+    return nh_kernel_name(dtype, n);
+}
+
+const char* hpdinv_method_kernel_name(int method, int dtype, int n) {
+    if (n < 1 || n > HPDINV_MAX_N || dtype < 0 || dtype > 1) return nullptr;
+    return base_kernel_name(method, dtype, n);
+}
+
 const char* hpdinv_solve_kernel_name(int method, int dtype, int n) {
     if (n < 1 || n > HPDINV_MAX_N || dtype < 0 || dtype > 1) return nullptr;
     return solve_kernel_name(dtype, method != 0, n);

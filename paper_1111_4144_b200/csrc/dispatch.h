@@ -42,6 +42,10 @@ int launch_grp(int dtype, bool ldl, const LaunchArgs& a);       // k_grp.cu (int
 int launch_blk(int dtype, bool ldl, const LaunchArgs& a);       // k_blk.cu (n = 32, 64)
 int launch_solve(int dtype, bool ldl, const SolveArgs& a);      // k_solve.cu (any n <= 64)
 const char* solve_kernel_name(int dtype, bool ldl, int n);
+int launch_base(int method, int dtype, const LaunchArgs& a);    // k_base.cu (methods 2, 3)
+const char* base_kernel_name(int method, int dtype, int n);
+int launch_nh(int dtype, const LaunchArgs& a);                  // k_nh.cu (non-Hermitian, f2)
+const char* nh_kernel_name(int dtype, int n);
 
 // Largest n of each family per dtype (0 = c64, 1 = c128).
 constexpr int reg_max_n(int dtype) { return dtype == 0 ? 8 : 6; }

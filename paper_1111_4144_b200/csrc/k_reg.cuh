@@ -64,6 +64,38 @@ __device__ __forceinline__ int reg_factor(cplx<T> (&r)[N * (N + 1) / 2], T (&inv
     return inf;
 }
 
+// S3 / S4: the proposed inversion (eqs. 20-24 / 25-29), rows k = N-1..0, in place over the
+// factor's packed upper triangle (row k of X overwrites row k of R, App. A.1); x_kk real (R4).
+template <typename T, int N, bool LDL>
+__device__ __forceinline__ void reg_invert(cplx<T> (&r)[N * (N + 1) / 2], const T (&inv)[N]) {
+#pragma unroll
+    for (int k = N - 1; k >= 0; k--) {
+        cplx<T> t[N];
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+            if (j <= k) continue;
+            cplx<T> s = czero<T>();
+#pragma unroll
+            for (int m = 0; m < N; m++) {
+                if (m <= k) continue;
+                const cplx<T> xmj = (m <= j) ? r[upk(N, m, j)] : conjz(r[upk(N, j, m)]);
+                cfma(s, r[upk(N, k, m)], xmj);
+            }
+            t[j] = LDL ? mk<T>(-s.x, -s.y) : cscale(s, -inv[k]);
+        }
+        T s = T(0);
+#pragma unroll
+        for (int m = 0; m < N; m++)
+            if (m > k) s = re_dot_conj(s, r[upk(N, k, m)], t[m]);
+        const T xkk = LDL ? inv[k] - s : inv[k] * (inv[k] - s);
+        r[upk(N, k, k)] = mk<T>(xkk, T(0));
+#pragma unroll
+        for (int j = 0; j < N; j++)
+            if (j > k) r[upk(N, k, j)] = t[j];
+    }
+
+}
+
 template <typename T, int N, bool LDL>
 __global__ void __launch_bounds__(kRegThreads)
 k_reg(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
@@ -90,32 +122,8 @@ k_reg(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
     // ---- S2: factorisation
     const int inf = reg_factor<T, N, LDL>(r, inv);
 
-    // ---- S3/S4: proposed inversion, rows k = N-1..0, in place over R's upper triangle
-#pragma unroll
-    for (int k = N - 1; k >= 0; k--) {
-        cplx<T> t[N];
-#pragma unroll
-        for (int j = 0; j < N; j++) {
-            if (j <= k) continue;
-            cplx<T> s = czero<T>();
-#pragma unroll
-            for (int m = 0; m < N; m++) {
-                if (m <= k) continue;
-                const cplx<T> xmj = (m <= j) ? r[upk(N, m, j)] : conjz(r[upk(N, j, m)]);
-                cfma(s, r[upk(N, k, m)], xmj);
-            }
-            t[j] = LDL ? mk<T>(-s.x, -s.y) : cscale(s, -inv[k]);
-        }
-        T s = T(0);
-#pragma unroll
-        for (int m = 0; m < N; m++)
-            if (m > k) s = re_dot_conj(s, r[upk(N, k, m)], t[m]);
-        const T xkk = LDL ? inv[k] - s : inv[k] * (inv[k] - s);
-        r[upk(N, k, k)] = mk<T>(xkk, T(0));
-#pragma unroll
-        for (int j = 0; j < N; j++)
-            if (j > k) r[upk(N, k, j)] = t[j];
-    }
+    // ---- S3/S4: proposed inversion
+    reg_invert<T, N, LDL>(r, inv);
 
     // ---- S5: mirror + store
     cplx<T>* Xb = X + b * sXm;

@@ -37,7 +37,7 @@ class Config:
     divisor: float = 1.0   # A = B B^H / divisor + delta I
     delta: float = 0.0
     desc: str = ""
-    task: str = "inv"      # "inv" (the hot path) | "solve" (A x = y)
+    task: str = "inv"      # "inv" (the hot path) | "solve" (§8(f) f1: A x = y) | "nonherm" (f2)
 
     @property
     def elem_bytes(self) -> int:
@@ -60,6 +60,11 @@ CONFIGS = {
     6: Config(6, 8, torch.complex64, 1 << 20, "chol", "soa", "bbh", 8.0, 0.1,
               "2^20 c64 HPD 8x8 systems A x = y (cfg2 matrices, y ~ CN(0,I)), Cholesky solve eqs. 5-7, "
               "interleaved", task="solve"),
+    # SURVEY §8(f) f2 (next row): non-Hermitian D = I + B / (2 sqrt(n)), B i.i.d. CN(0,1) (a
+    # channel-like matrix near the identity; the paper gives no workload), D^-1 = D* (DD*)^-1
+    7: Config(7, 8, torch.complex64, 1 << 20, "chol", "soa", "nonherm", 2.0 * 8 ** 0.5, 1.0,
+              "2^20 c64 non-Hermitian 8x8 D = I + B/(2 sqrt 8), D^-1 = D*(DD*)^-1 (P:135-141), interleaved",
+              task="nonherm"),
 }
 
 
@@ -88,6 +93,9 @@ def _gen_chunk(cfg: Config, chunk: int, count: int, device, seed: int) -> torch.
         A = torch.matmul(B, B.conj().transpose(-1, -2)) / cfg.divisor
         A = A + cfg.delta * torch.eye(n, dtype=cfg.dtype, device=device)
         return _hermitise(A)
+    if cfg.kind == "nonherm":            # D = delta I + B / divisor (not Hermitian)
+        B = torch.randn(count, n, n, dtype=cfg.dtype, device=device, generator=g)
+        return B / cfg.divisor + cfg.delta * torch.eye(n, dtype=cfg.dtype, device=device)
     # spectral: A = Q diag(lam) Q^H
     G = torch.randn(count, n, n, dtype=cfg.dtype, device=device, generator=g)
     U = torch.rand(count, n, dtype=torch.float64, device=device, generator=g)

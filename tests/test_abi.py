@@ -64,6 +64,23 @@ def test_validation_without_gpu(lib):
     assert lib.hpdinv_solve_kernel_name(0, 0, 8) == b"k_solve_reg<c64,chol>"
     assert lib.hpdinv_solve_kernel_name(1, 1, 64) == b"k_solve_gen<c128,ldl>"
     assert lib.hpdinv_solve_kernel_name(0, 0, 65) is None
+    # existing methods (f3): argument k of the 10-argument form is k + 2
+    assert lib.hpdinv_inv_batched_method(4, 0, 4, 8, fake, 1, 4, fake, 1, 4, fake, z) == -1
+    assert lib.hpdinv_inv_batched_method(2, 2, 4, 8, fake, 1, 4, fake, 1, 4, fake, z) == -2
+    assert lib.hpdinv_inv_batched_method(2, 0, -1, 8, fake, 1, 4, fake, 1, 4, fake, z) == -3
+    assert lib.hpdinv_inv_batched_method(3, 1, 4, 0, fake, 1, 4, fake, 1, 4, fake, z) == -4
+    assert lib.hpdinv_inv_batched_method(0, 0, 4, 8, z, 1, 4, fake, 1, 4, fake, z) == -5
+    assert lib.hpdinv_inv_batched_method(2, 0, 0, 8, z, 1, 4, z, 1, 4, z, z) == 0
+    assert lib.hpdinv_method_kernel_name(2, 0, 8) == b"k_base_reg<c64,eqsolve>"
+    assert lib.hpdinv_method_kernel_name(3, 1, 33) == b"k_base_gen<c128,trimat>"
+    assert lib.hpdinv_method_kernel_name(0, 0, 8) is None
+    # non-Hermitian inversion (f2): the 10-argument convention
+    assert lib.nonherm_inv_batched_c64(0, 8, z, 1, 0, z, 1, 0, z, z) == 0
+    assert lib.nonherm_inv_batched_c128(4, 0, fake, 1, 4, fake, 1, 4, fake, z) == -2
+    assert lib.nonherm_inv_batched_c64(4, 8, fake, 2, 2, fake, 1, 4, fake, z) == -4
+    assert lib.nonherm_inv_batched_c64(4, 8, fake, 1, 4, fake, 1, 4, z, z) == -9
+    assert lib.hpdinv_nonherm_kernel_name(0, 8) == b"k_nh_reg<c64>"
+    assert lib.hpdinv_nonherm_kernel_name(1, 8) == b"k_nh_gen<c128>"
 
 
 def test_no_cpu_fallback_in_product_path():

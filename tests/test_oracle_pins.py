@@ -343,6 +343,33 @@ def test_nonhermitian(orc):
         assert np.abs(Di - Xe).max() <= 1e-10 * np.abs(Xe).max() * np.linalg.cond(D) ** 2 * 1e-2
 
 
+def test_nonhermitian_batched(orc):
+    """The batched driver equals per-matrix calls; on exactly invertible Gaussian-integer D
+    (unit upper bidiagonal {+-1, +-i} times a signed permutation) D^-1 is checked against the
+    exact inverse, and against numpy.linalg.inv on random D."""
+    rng = np.random.default_rng(11)
+    Ds = []
+    for _ in range(20):
+        n = 6
+        U = np.eye(n, dtype=complex)
+        U[np.arange(n - 1), np.arange(1, n)] = np.array([1, -1, 1j, -1j])[rng.integers(0, 4, n - 1)]
+        P = np.eye(n)[rng.permutation(n)] * rng.choice([-1, 1], n)
+        Ds.append(P @ U)
+    Ds = np.array(Ds)
+    Dinv, info = orc.nonherm_batched(Ds)
+    assert (info == 0).all()
+    for b in range(len(Ds)):
+        np.testing.assert_allclose(Dinv[b] @ Ds[b], np.eye(6), atol=1e-12)
+        one, i1 = orc.nonhermitian_inv(Ds[b])
+        assert np.array_equal(one, Dinv[b]) and i1 == info[b]
+    D = rng.standard_normal((7, 5, 5)) + 1j * rng.standard_normal((7, 5, 5)) + 2 * np.eye(5)
+    Dinv, info = orc.nonherm_batched(D)
+    np.testing.assert_allclose(Dinv, np.linalg.inv(D), rtol=0, atol=1e-11)
+    Dz = np.zeros((1, 3, 3), complex)
+    Dinv, info = orc.nonherm_batched(Dz)
+    assert info[0] == 1 and np.isnan(Dinv).all()
+
+
 # ---------------------------------------------------------------------- batched + strides
 def test_batched_layouts(orc):
     """The strided batched driver equals the single-matrix routines, for AoS and SoA
