@@ -185,6 +185,8 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     B = cfg.batch
+    if cfg.task == "fxp":
+        return run_fxp(args, cfg, rank, world, dev)
     A = wl.generate(cfg, rank * B, B, device=dev, seed=args.seed)   # this rank's slice
     store, view = wl.to_layout(A, cfg.layout)
     del A
@@ -358,6 +360,83 @@ def run_ours(args, rank, world, local_rank):
     return out
 
 
+# ------------------------------------------- f4: fixed-point emulation of the §IV.C study
+def run_fxp(args, cfg, rank, world, dev):
+    """Times hpdinv_fxp_inv_batched (the proposed method in Q(qm, qf) integer emulation) over
+    the cfg8 batch, and reports the study itself: mean relative error of the three methods vs
+    the double-precision inverse on a sample of the GPU results (Fig. 1)."""
+    import paper_1111_4144_b200 as hp
+    B = cfg.batch
+    A, raw = wl.generate_fxp(cfg, rank * B, B, device=dev, seed=args.seed)
+    X = torch.empty_like(raw)
+    info = torch.empty(B, dtype=torch.int32, device=dev)
+    nsat = torch.empty(B, dtype=torch.int64, device=dev)
+    steps = args.steps if args.steps is not None else 10
+    warmup = max(3, args.warmup)
+    for _ in range(warmup):
+        hp.fxp_invert(raw, cfg.qm, cfg.qf, "proposed", X, info, nsat)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier(device_ids=[dev.index])
+    sampler = ClockSampler(torch.cuda.current_device())
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler.start()
+    a.record()
+    for _ in range(steps):
+        hp.fxp_invert(raw, cfg.qm, cfg.qf, "proposed", X, info, nsat)
+    b.record()
+    torch.cuda.synchronize()
+    sampler.stop()
+    t = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = t.item()
+    # the study on a sample (host double-precision reference)
+    S = min(B, 4096)
+    Xr = np.linalg.inv(A[:S].cpu().numpy())
+    study = {}
+    for method in ("proposed", "eqsolve", "trimat"):
+        Xm, im, sm = hp.fxp_invert(raw[:S].contiguous(), cfg.qm, cfg.qf, method)
+        torch.cuda.synchronize()
+        Xm, im, sm = Xm.cpu().numpy(), im.cpu().numpy(), sm.cpu().numpy()
+        ok = (im == 0) & (sm == 0)
+        Xf = Xm[..., 0] / 2.0 ** cfg.qf + 1j * Xm[..., 1] / 2.0 ** cfg.qf
+        rel = np.linalg.norm((Xf - Xr)[ok], axis=(1, 2)) / np.linalg.norm(Xr[ok], axis=(1, 2))
+        Af = A[:S].cpu().numpy()[ok]
+        res = np.linalg.norm(Af @ Xf[ok] - np.eye(cfg.n), axis=(1, 2))
+        study[method] = {"mean_rel_err": float(rel.mean()), "mean_residual": float(res.mean()),
+                         "failures": int((~ok).sum()), "trials": S}
+    pk = peaks()
+    byts = 2 * 16 * cfg.n * cfg.n * B + 12 * B
+    achieved = byts / (ms / 1e3) / 1e9
+    out = {
+        "metric": "fixed-point Q%d.%d emulated inversions/sec (SURVEY 8(f) f4, P:206-208), 1 B200" % (cfg.qm, cfg.qf),
+        "value": world * B / (ms / 1e3), "unit": "matrices/s", "n_gpus": world, "steps": steps,
+        "warmup": warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64 (Q%d.%d raws, 128-bit products)" % (cfg.qm, cfg.qf),
+        "data": "synthetic (SPEC.md ensemble, seeded, chunk-keyed)",
+        "config": {"workload": "cfg%d: %s" % (cfg.cid, cfg.desc), "n": cfg.n, "batch_per_gpu": B,
+                   "task": "fxp", "format": "Q%d.%d" % (cfg.qm, cfg.qf),
+                   "l2": "inputs larger than L2" if byts > L2_BYTES else "working set fits L2"},
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "kernel": "k_fxp<%d>" % cfg.n, "kernel_ms": ms,
+                     "traffic": None, "note": "integer emulation (128-bit software products and "
+                     "divisions), ALU bound; the HBM fraction is shown for scale only"},
+        "study": study, "clocks": sampler.summary(), "gpu_launches": steps, "e2e": None,
+        "e2e_note": "no host-buffer entry point for this task",
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        n0 = 256
+        t0 = time.perf_counter()
+        oracle.fxp_inv_batched(raw[:n0].cpu().numpy(), cfg.qm, cfg.qf, "proposed")
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": n0 / dt, "unit": "matrices/s", "cores": oracle.max_threads(),
+                               "kind": "oracle", "sample": "first %d of the %d matrices of cfg8" % (n0, B)}
+    return out
+
+
 # ------------------------------------------------------- vendor-library comparison (context)
 def library_baseline(cfg: wl.Config, view, yview, dev, steps: int = 5):
     """The same workload through PyTorch's batched dense linear algebra on the same GPU
@@ -409,13 +488,18 @@ def library_baseline(cfg: wl.Config, view, yview, dev, steps: int = 5):
 # ------------------------------------------------------------------- the oracle arm
 def oracle_sample(cfg: wl.Config, count: int, seed: int, dev):
     """Host complex128 copy of the first `count` matrices of the workload (exact upcast of
-    the bits the GPU consumes when generated on the GPU)."""
+    the bits the GPU consumes when generated on the GPU); fixed-point raws for cfg8."""
+    if cfg.task == "fxp":
+        return wl.generate_fxp(cfg, 0, count, device=dev, seed=seed)[1].cpu().numpy()
     A = wl.generate(cfg, 0, count, device=dev, seed=seed)
     return A.cpu().to(torch.complex128).numpy()
 
 
 def oracle_run(cfg: wl.Config, Ah, yh):
     import oracle
+    if cfg.task == "fxp":
+        X, info, _ = oracle.fxp_inv_batched(Ah, cfg.qm, cfg.qf, "proposed")
+        return X, info
     if cfg.task == "nonherm":
         return oracle.nonherm_batched(Ah)
     if cfg.task == "solve":

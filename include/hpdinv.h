@@ -176,6 +176,24 @@ int nonherm_inv_batched_c128(int64_t batch, int n,
 const char *hpdinv_nonherm_kernel_name(int dtype, int n);
 
 /* ---------------------------------------------------------------------------------------
+ * Fixed-point (Q-format) emulation of the inversion methods for the paper's accuracy study
+ * (§IV.C, Fig. 1).  The paper fixes no format; the arithmetic
+ * is DESIGN.md's reading F1-F7 (Q(m, f) raws, saturation, one round-half-even per F4 product
+ * component, round-half-even division by the pivot, exact rounded square root, term-by-term
+ * accumulation).  method: 0 proposed (Cholesky + eqs. 20-24), 1 equation solving (eq. 15),
+ * 2 triangular matrix operations (eqs. 16-19).
+ *   A, X: device, contiguous batch x n x n, each complex entry an interleaved (re, im) pair of
+ *     int64 raws (value = raw * 2^-f); only the upper triangle and Re a_ii of A are read; X is
+ *     written in full (Hermitian mirror) and is zero when info != 0.
+ *   info[b]: first 1-based pivot with a non-positive radicand, else 0; nsat[b]: number of
+ *     saturation events in matrix b (int64).
+ * 1 <= m, 1 <= f, m + f <= 40; 1 <= n <= 16.  Returns 0, -k for invalid argument k (1 method,
+ * 2 the format (m, f), 4 batch, 5 n, 6 A, 7 X, 8 info, 9 nsat), or a cudaError_t.
+ * One matrix per thread, integer ALU; asynchronous, stream-ordered, no allocation. */
+int hpdinv_fxp_inv_batched(int method, int m, int f, int64_t batch, int n, const int64_t *A,
+                           int64_t *X, int32_t *info, int64_t *nsat, cudaStream_t stream);
+
+/* ---------------------------------------------------------------------------------------
  * Host-buffer entry point (end-to-end use from host memory).
  *
  * hpdinv_inv_host runs the same hot path on matrices that live in HOST memory (pinned

@@ -24,6 +24,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "hpdinv_oracle.c")
 _HDR = os.path.join(_HERE, "hpdinv_oracle.h")
 _LIB = os.path.join(_HERE, "liboracle.so")
+_FXP_SRC = os.path.join(_HERE, "fxp_oracle.c")      # fixed-point emulation
+_FXP_HDR = os.path.join(_HERE, "fxp_oracle.h")
 
 PAPER_CONVENTION = 0
 FULL_EXPLOITATION = 1
@@ -41,12 +43,12 @@ class Counts(ctypes.Structure):
 
 def build(force: bool = False) -> str:
     """Compile ``liboracle.so`` with gcc (plain -O2, OpenMP across matrices only)."""
-    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))
+    newest = max(os.path.getmtime(p) for p in (_SRC, _HDR, _FXP_SRC, _FXP_HDR))
     if not force and os.path.exists(_LIB) and os.path.getmtime(_LIB) >= newest:
         return _LIB
     tmp = _LIB + ".tmp%d" % os.getpid()
     cmd = ["gcc", "-O2", "-std=c11", "-fopenmp", "-ffp-contract=off", "-fPIC", "-shared",
-           "-o", tmp, _SRC, "-lm"]
+           "-o", tmp, _SRC, _FXP_SRC, "-lm"]
     subprocess.check_call(cmd)
     os.replace(tmp, _LIB)
     return _LIB
@@ -78,6 +80,8 @@ def lib() -> ctypes.CDLL:
             "oracle_solve_batched": (I, [I64, I, P, I64, I64, P, P, P, I, I]),
             "oracle_nonherm_batched": (I, [I64, I, P, P, P, I]),
             "oracle_max_threads": (I, []),
+            "oracle_fxp_inv_batched": (I, [I64, I, P, P, P, P, I, I, I, I]),
+            "oracle_fxp_op": (I, [I, I, I, I64, I64, I64, I64, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -251,6 +255,32 @@ def nonherm_batched(D: np.ndarray, nthreads: int = 0):
     if rc != 0:
         raise ValueError("oracle_nonherm_batched rejected its arguments (rc=%d)" % rc)
     return Dinv, info
+
+
+FXP_METHODS = {"proposed": 0, "eqsolve": 1, "trimat": 2}
+
+
+def fxp_inv_batched(A_raw: np.ndarray, m: int, f: int, method: str = "proposed", nthreads: int = 0):
+    """Fixed-point Q(m, f) emulation.  A_raw: (batch, n, n, 2) int64 raws.
+    Returns (X_raw (batch, n, n, 2) int64, info int32, nsat int64)."""
+    A = np.ascontiguousarray(A_raw, dtype=np.int64)
+    batch, n = A.shape[0], A.shape[1]
+    X = np.zeros_like(A)
+    info = np.zeros(batch, np.int32)
+    nsat = np.zeros(batch, np.int64)
+    rc = lib().oracle_fxp_inv_batched(batch, n, _ptr(A), _ptr(X), _ptr(info), _ptr(nsat), m, f,
+                                      FXP_METHODS[method], int(nthreads))
+    if rc != 0:
+        raise ValueError("oracle_fxp_inv_batched rejected its arguments (rc=%d)" % rc)
+    return X, info, nsat
+
+
+def fxp_op(op: str, m: int, f: int, a, b=(0, 0)):
+    """One F4 product ('mul'), F5 quotient ('div', b = (p, 0)) or F6 root ('sqrt') on raws."""
+    out = np.zeros(2, np.int64)
+    ns = lib().oracle_fxp_op({"mul": 0, "div": 1, "sqrt": 2}[op], m, f, int(a[0]), int(a[1]),
+                             int(b[0]), int(b[1]), _ptr(out))
+    return (int(out[0]), int(out[1])), int(ns)
 
 
 def max_threads() -> int:

@@ -22,7 +22,7 @@ __all__ = [
     "ldl_inv_batched_c128", "chol_solve_batched_c64", "chol_solve_batched_c128",
     "ldl_solve_batched_c64", "ldl_solve_batched_c128", "solve", "solve_kernel_name", "invert",
     "invert_method", "method_kernel_name", "nonherm_inv_batched_c64", "nonherm_inv_batched_c128",
-    "invert_nonhermitian", "nonherm_kernel_name", "invert_host", "host_workspace_bytes", "kernel_name", "version", "HpdinvError",
+    "invert_nonhermitian", "nonherm_kernel_name", "fxp_invert", "invert_host", "host_workspace_bytes", "kernel_name", "version", "HpdinvError",
 ]
 
 
@@ -191,6 +191,29 @@ def invert_nonhermitian(D, Dinv=None, info=None, stream=None):
 def nonherm_kernel_name(dtype: torch.dtype, n: int):
     r = lib().hpdinv_nonherm_kernel_name({torch.complex64: 0, torch.complex128: 1}[dtype], n)
     return r.decode() if r else None
+
+
+FXP_METHODS = {"proposed": 0, "eqsolve": 1, "trimat": 2}
+
+
+def fxp_invert(A_raw: torch.Tensor, m: int, f: int, method: str = "proposed", X=None, info=None,
+               nsat=None, stream=None):
+    """Fixed-point Q(m, f) emulation on the GPU: A_raw is a contiguous CUDA
+    int64 tensor (batch, n, n, 2) of raws.  Returns (X_raw, info, nsat)."""
+    if A_raw.dtype != torch.int64 or not A_raw.is_cuda or not A_raw.is_contiguous():
+        raise ValueError("fxp_invert: A_raw must be a contiguous CUDA int64 tensor (batch, n, n, 2)")
+    batch, n = A_raw.shape[0], A_raw.shape[1]
+    X = torch.empty_like(A_raw) if X is None else X
+    info = torch.empty(batch, dtype=torch.int32, device=A_raw.device) if info is None else info
+    nsat = torch.empty(batch, dtype=torch.int64, device=A_raw.device) if nsat is None else nsat
+    rc = lib().hpdinv_fxp_inv_batched(FXP_METHODS[method], m, f, batch, n, ctypes.c_void_p(A_raw.data_ptr()),
+                                      ctypes.c_void_p(X.data_ptr()), ctypes.c_void_p(info.data_ptr()),
+                                      ctypes.c_void_p(nsat.data_ptr()), ctypes.c_void_p(_stream_handle(stream)))
+    if rc < 0:
+        raise ValueError("hpdinv_fxp_inv_batched rejected argument %d" % (-rc))
+    if rc > 0:
+        raise HpdinvError("hpdinv_fxp_inv_batched: CUDA error %d at launch" % rc)
+    return X, info, nsat
 
 
 METHOD_IDS = {"chol": 0, "ldl": 1, "eqsolve": 2, "trimat": 3}

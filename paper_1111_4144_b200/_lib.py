@@ -41,6 +41,8 @@ def lib() -> ctypes.CDLL:
         f.argtypes = inv_args
     L.hpdinv_nonherm_kernel_name.restype = ctypes.c_char_p
     L.hpdinv_nonherm_kernel_name.argtypes = [I, I]
+    L.hpdinv_fxp_inv_batched.restype = I
+    L.hpdinv_fxp_inv_batched.argtypes = [I, I, I, I64, I, P, P, P, P, P]
     L.hpdinv_inv_batched_method.restype = I
     L.hpdinv_inv_batched_method.argtypes = [I, I] + inv_args
     L.hpdinv_method_kernel_name.restype = ctypes.c_char_p
@@ -68,6 +70,7 @@ EXPORTS = (
     "ldl_solve_batched_c64", "ldl_solve_batched_c128", "hpdinv_solve_kernel_name",
     "hpdinv_inv_batched_method", "hpdinv_method_kernel_name",
     "nonherm_inv_batched_c64", "nonherm_inv_batched_c128", "hpdinv_nonherm_kernel_name",
+    "hpdinv_fxp_inv_batched",
     "hpdinv_host_workspace_bytes", "hpdinv_inv_host",
     "hpdinv_kernel_name", "hpdinv_version",
 )

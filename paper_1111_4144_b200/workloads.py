@@ -37,7 +37,9 @@ class Config:
     divisor: float = 1.0   # A = B B^H / divisor + delta I
     delta: float = 0.0
     desc: str = ""
-    task: str = "inv"      # "inv" (the hot path) | "solve" (§8(f) f1: A x = y) | "nonherm" (f2)
+    task: str = "inv"      # "inv" (the hot path) | "solve" (§8(f) f1: A x = y) | "nonherm" (f2) | "fxp" (f4)
+    qm: int = 2            # fixed-point format Q(qm, qf) of the f4 study
+    qf: int = 13
 
     @property
     def elem_bytes(self) -> int:
@@ -65,6 +67,13 @@ CONFIGS = {
     7: Config(7, 8, torch.complex64, 1 << 20, "chol", "soa", "nonherm", 2.0 * 8 ** 0.5, 1.0,
               "2^20 c64 non-Hermitian 8x8 D = I + B/(2 sqrt 8), D^-1 = D*(DD*)^-1 (P:135-141), interleaved",
               task="nonherm"),
+    # SURVEY §8(f) f4 (next row): the fixed-point accuracy study of §IV.C with 16-bit words
+    # Q4.11 (reading F8: SPEC's Q2.13 saturates X = A^-1 in ~80 % of trials, |x| ~ 1/0.1),
+    # n = 16, SPEC.md's ensemble: G re/im ~ U[-1, 1], A = G G^H / n + 0.1 I, scaled
+    # so max |a_ij| <= 0.9 * (2^m - 2^-f), then quantized (round half to even, saturated)
+    8: Config(8, 16, torch.complex128, 1 << 16, "chol", "aos", "fxp", 16.0, 0.1,
+              "2^16 Q4.11 fixed-point HPD 16x16 (SPEC ensemble), Cholesky + proposed inversion emulated "
+              "in integer arithmetic (F1-F7)", task="fxp", qm=4, qf=11),
 }
 
 
@@ -156,6 +165,43 @@ def vec_layout(Y: torch.Tensor, layout: str, ld: Optional[int] = None) -> Tuple[
     if ld > batch:
         planes[:, batch:] = float("nan")
     return planes, torch.as_strided(planes, (batch, n), (1, ld))
+
+
+def quantize(x: torch.Tensor, m: int, f: int) -> torch.Tensor:
+    """Real tensor -> int64 raws of Q(m, f): round half to even of x 2^f (torch.round), saturated
+    to [-2^(m+f), 2^(m+f) - 1] (SPEC.md quantize; DESIGN reading F1-F2)."""
+    r = torch.round(x.to(torch.float64) * float(2 ** f))
+    return r.clamp(-float(2 ** (m + f)), float(2 ** (m + f) - 1)).to(torch.int64)
+
+
+def generate_fxp(cfg: Config, start: int = 0, count: Optional[int] = None, device="cpu",
+                 seed: int = 0) -> Tuple[torch.Tensor, torch.Tensor]:
+    """f4 study inputs: (A complex128 (count, n, n) -- the unquantized matrices the double
+    reference inverts -- and A_raw int64 (count, n, n, 2), its Q(qm, qf) quantization).
+    Chunk-keyed like `generate`."""
+    if count is None:
+        count = cfg.batch - start
+    n = cfg.n
+    out = torch.empty(count, n, n, dtype=torch.complex128, device=device)
+    rho = 0.9 * (2.0 ** cfg.qm - 2.0 ** -cfg.qf)
+    pos = start
+    while pos < start + count:
+        c = pos // CHUNK
+        c0 = c * CHUNK
+        take = min(c0 + CHUNK, start + count) - pos
+        g = torch.Generator(device=device)
+        g.manual_seed(chunk_seed(seed, cfg.cid, c))
+        U = torch.rand(CHUNK, n, n, 2, dtype=torch.float64, device=device, generator=g) * 2.0 - 1.0
+        G = torch.complex(U[..., 0], U[..., 1])
+        A = torch.matmul(G, G.conj().transpose(-1, -2)) / cfg.divisor
+        A = A + cfg.delta * torch.eye(n, dtype=torch.complex128, device=device)
+        A = _hermitise(A)
+        mx = A.abs().amax(dim=(1, 2))
+        A = A / torch.clamp(mx / rho, min=1.0)[:, None, None]
+        out[pos - start:pos - start + take] = A[pos - c0:pos - c0 + take]
+        pos += take
+    raw = torch.stack([quantize(out.real, cfg.qm, cfg.qf), quantize(out.imag, cfg.qm, cfg.qf)], dim=-1)
+    return out, raw.contiguous()
 
 
 def soa_view(planes: torch.Tensor, batch: int, n: int) -> torch.Tensor:

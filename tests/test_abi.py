@@ -81,6 +81,13 @@ def test_validation_without_gpu(lib):
     assert lib.nonherm_inv_batched_c64(4, 8, fake, 1, 4, fake, 1, 4, z, z) == -9
     assert lib.hpdinv_nonherm_kernel_name(0, 8) == b"k_nh_reg<c64>"
     assert lib.hpdinv_nonherm_kernel_name(1, 8) == b"k_nh_gen<c128>"
+    # fixed-point emulation (f4)
+    assert lib.hpdinv_fxp_inv_batched(3, 4, 11, 4, 8, fake, fake, fake, fake, z) == -1
+    assert lib.hpdinv_fxp_inv_batched(0, 30, 11, 4, 8, fake, fake, fake, fake, z) == -2
+    assert lib.hpdinv_fxp_inv_batched(0, 4, 11, -1, 8, fake, fake, fake, fake, z) == -4
+    assert lib.hpdinv_fxp_inv_batched(0, 4, 11, 4, 17, fake, fake, fake, fake, z) == -5
+    assert lib.hpdinv_fxp_inv_batched(0, 4, 11, 4, 8, z, fake, fake, fake, z) == -6
+    assert lib.hpdinv_fxp_inv_batched(1, 4, 11, 0, 8, z, z, z, z, z) == 0
 
 
 def test_no_cpu_fallback_in_product_path():
