@@ -42,12 +42,21 @@ struct GrpShape {
     static constexpr int G = G_;                      // lanes per matrix
     static constexpr int C = (N + G - 1) / G;         // columns per lane
     static constexpr int MPW = 32 / G;                // matrices per warp
-    static constexpr int WARPS = 4;
+#ifndef HPDINV_GRP_WARPS16
+#define HPDINV_GRP_WARPS16 4
+#endif
+#ifndef HPDINV_GRP_WARPS32
+#define HPDINV_GRP_WARPS32 8
+#endif
+    // n = 32: one 8-warp CTA per SM (248 registers) keeps the SM's warps in the same phase of
+    // the 130 KB unrolled code (i-cache): 8.0 -> 7.5 ms at cfg5 against two 4-warp CTAs;
+    // forcing lockstep with __syncthreads every 4/8/16 steps measured slower (8.1-8.5 ms)
+    static constexpr int WARPS = N <= 16 ? HPDINV_GRP_WARPS16 : HPDINV_GRP_WARPS32;
     static constexpr int THREADS = 32 * WARPS;
     static constexpr int MPC = MPW * WARPS;           // matrices per CTA
     // n <= 16: 3 CTAs/SM caps ptxas at 170 registers (12 warps/SM); n = 32 (two 32-row columns
     // per lane) runs 8 warps/SM with up to 255 registers instead of spilling (measured faster)
-    static constexpr int MIN_BLOCKS = N <= 16 ? 3 : 2;
+    static constexpr int MIN_BLOCKS = N <= 16 ? (12 / WARPS > 0 ? 12 / WARPS : 1) : (8 / WARPS > 0 ? 8 / WARPS : 1);
     static constexpr int P = sizeof(T) == 4 ? 2 : 1;  // complex elements per 16-byte load
     // packed row store: row i holds j = i..n-1 at offset roff(i) + (j - i), 16-byte aligned
     __host__ __device__ static constexpr int rlen(int i) { return ((N - i) + P - 1) / P * P; }
