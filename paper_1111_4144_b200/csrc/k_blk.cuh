@@ -54,10 +54,11 @@ struct BlkShape {
 
 namespace blk {
 #ifdef HPDINV_BLK_PROF
-__device__ unsigned long long g_prof[16];      // per-phase cycles of thread 0, summed over CTAs
+__device__ unsigned long long g_prof[2][16];   // per-phase cycles, summed over CTAs, of lane 0 of
+                                               // [0] the serial warp and [1] the next warp
 #define BLK_PHASE(id)                                             \
     do {                                                          \
-        if (threadIdx.x == 0) {                                   \
+        if (prof_on_) {                                           \
             const long long t_ = clock64();                       \
             prof_[prof_cur_] += t_ - prof_t_;                     \
             prof_t_ = t_;                                         \
@@ -239,6 +240,8 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
     long long prof_[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // F1 F2a F2b I1 I2 I3 I4 S5 - S1
     long long prof_t_ = clock64();
     int prof_cur_ = 9;                                  // 9 = S1 (load)
+    const int prof_role_ = (warp == swarp) ? 0 : 1;
+    const bool prof_on_ = lane == 0 && (warp == swarp || warp == (swarp + 1) % (NT / 32));
 #endif
     // ------------------------------------------------------------------ S1: upper(A) -> W
     for (int e = tid; e < N * N; e += NT) {
@@ -260,6 +263,8 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
         if constexpr (Sh::LA) {
             // lookahead: the serial warp computes the diagonal block of P and factors it (F2a)
             // while the other warps compute the rest of the panel (nothing below depends on it)
+            // (computing the diagonal block's F1 by all warps first, with split chains, measured
+            // slower: the extra barrier costs more than the serial warp's longer chains)
             if (warp == swarp) {
                 if (k0 > 0) blk::f1<T, N, LDW, RT, Sh::CTD>(W, k0, lane % PR, lane / PR, k0, k0 + NB);
                 __syncwarp();
@@ -499,8 +504,8 @@ k_blk(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
     if (tid == 0) info[b] = inf;
 #ifdef HPDINV_BLK_PROF
     BLK_PHASE(8);
-    if (tid == 0)
-        for (int i = 0; i < 10; i++) atomicAdd(&blk::g_prof[i], (unsigned long long)prof_[i]);
+    if (prof_on_)
+        for (int i = 0; i < 10; i++) atomicAdd(&blk::g_prof[prof_role_][i], (unsigned long long)prof_[i]);
 #endif
 #undef WE
 }

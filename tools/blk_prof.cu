@@ -26,22 +26,26 @@ void run(const char* name, int64_t batch) {
     auto fn = k_blk<T, N, NB, LDL, NT, RT>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Sh::smem_bytes));
     fn<<<unsigned(batch), NT, Sh::smem_bytes>>>(batch, A, N * N, 1, X, N * N, 1, info);   // warm-up
-    unsigned long long z[16] = {0};
+    unsigned long long z[32] = {0};
     cudaMemcpyToSymbol(blk::g_prof, z, sizeof(z));
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
     fn<<<unsigned(batch), NT, Sh::smem_bytes>>>(batch, A, N * N, 1, X, N * N, 1, info);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
-    unsigned long long p[16];
+    unsigned long long p[32];
     cudaMemcpyFromSymbol(p, blk::g_prof, sizeof(p));
     const char* names[10] = {"F1", "F2a", "F2b", "I1", "I2", "I3", "I4", "S5", "-", "S1"};
-    unsigned long long tot = 0;
-    for (int i = 0; i < 10; i++) tot += p[i];
-    printf("%s batch=%lld  %.3f ms  (%s)  cycles/matrix (thread 0): %.0f\n", name, (long long)batch, ms,
-           cudaGetErrorString(cudaGetLastError()), double(tot) / batch);
-    for (int i = 0; i < 10; i++)
-        if (p[i]) printf("  %-4s %9.0f cyc/matrix  %5.1f %%\n", names[i], double(p[i]) / batch, 100.0 * p[i] / tot);
+    for (int role = 0; role < (NT > 32 ? 2 : 1); role++) {
+        unsigned long long tot = 0;
+        for (int i = 0; i < 10; i++) tot += p[role * 16 + i];
+        printf("%s batch=%lld  %.3f ms  (%s)  %s warp, cycles/matrix (lane 0): %.0f\n", name, (long long)batch, ms,
+               cudaGetErrorString(cudaGetLastError()), role == 0 ? "serial" : "GEMM", double(tot) / batch);
+        for (int i = 0; i < 10; i++)
+            if (p[role * 16 + i])
+                printf("  %-4s %9.0f cyc/matrix  %5.1f %%\n", names[i], double(p[role * 16 + i]) / batch,
+                       100.0 * p[role * 16 + i] / tot);
+    }
     cudaFree(A); cudaFree(X); cudaFree(info);
 }
 
