@@ -71,6 +71,12 @@ struct GrpShape {
 };
 
 namespace grp {
+// X is streamed out and never re-read: evict-first stores (measured ~1 % faster at cfg3 and
+// cfg5; evict-first LOADS cost 7 % at cfg5, where neighbouring lanes share AoS sectors in L1)
+template <typename V>
+__device__ __forceinline__ void st(V* p, V v) { __stcs(p, v); }
+template <typename V>
+__device__ __forceinline__ V ld(const V* p) { return __ldg(p); }
 template <typename T>
 __device__ __forceinline__ void lds_pair(const cplx<T>* p, int o, cplx<T>& e0, cplx<T>& e1) {
     if constexpr (sizeof(T) == 4) {
@@ -121,7 +127,7 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
             for (int l = 0; l < N; l++) {
                 col[s][l] = czero<T>();
                 if (l <= G * s + G - 1 && l <= j && j < N)
-                    col[s][l] = __ldg(reinterpret_cast<const V*>(Ab + uint64_t(uint32_t(l * N + G * s)) * seA));
+                    col[s][l] = grp::ld(reinterpret_cast<const V*>(Ab + uint64_t(uint32_t(l * N + G * s)) * seA));
             }
         }
     }
@@ -258,7 +264,7 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
             if (j < N) {
 #pragma unroll
                 for (int m = 0; m < N; m++)
-                    *reinterpret_cast<V*>(Xrow + uint64_t(uint32_t(m * N + G * s)) * seX) = col[s][m];
+                    grp::st(reinterpret_cast<V*>(Xrow + uint64_t(uint32_t(m * N + G * s)) * seX), col[s][m]);
             }
         }
         if (inf) {          // a flagged matrix is overwritten (same thread, program order)

@@ -97,3 +97,13 @@ def test_singular_flagged(orc):
     assert infoo[5] > 0
     assert np.array_equal(infog[[5]], infoo[[5]])
     assert np.isnan(Yg[5]).all()
+
+
+def test_padded_layouts_match(orc):
+    cfg = wl.CONFIGS[7]
+    D = wl.generate(cfg, 0, 1000, device="cuda")
+    Y1, i1 = hp.invert_nonhermitian(D)
+    _, Dv = wl.to_layout(D, "soa", ld=1000 + 24)
+    Y2, i2 = hp.invert_nonhermitian(Dv)
+    torch.cuda.synchronize()
+    assert torch.equal(Y1, Y2.contiguous()) and torch.equal(i1, i2)

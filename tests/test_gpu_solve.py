@@ -146,3 +146,22 @@ def test_full_size_sampled(orc):
         r -= Y[s:s + step].to(torch.complex128)
         rel = (r.abs().amax(1) / Y[s:s + step].abs().amax(1)).max().item()
         assert rel <= 1e-3, rel
+
+
+@pytest.mark.parametrize("n", [4, 8, 12])
+def test_inplace_padded_and_side_stream(orc, n):
+    """Xv aliasing Y with identical strides (header contract), padded interleaved ld for A and
+    the vectors, a non-default stream: same results as the plain call."""
+    cfg = wl.Config(93, n, torch.complex64, 0, "chol", "soa", "bbh", float(n), 0.1, task="solve")
+    B = 777
+    A = wl.generate(cfg, 0, B, device="cuda")
+    Y = wl.generate_rhs(cfg, 0, B, device="cuda")
+    ref, rinfo = hp.solve(A, Y.clone())
+    _, Av = wl.to_layout(A, "soa", ld=B + 37)
+    _, Yv = wl.vec_layout(Y, "soa", ld=B + 11)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        x, info = hp.solve(Av, Yv, "chol", Xv=Yv, stream=s)
+    s.synchronize()
+    assert x.data_ptr() == Yv.data_ptr()
+    assert torch.equal(x.contiguous(), ref.contiguous()) and torch.equal(info, rinfo)
