@@ -223,10 +223,10 @@ extern "C" int hpdinv_fxp_inv_batched(int method, int m, int f, int64_t batch, i
     if (batch < 0) return -4;
     if (n < 1 || n > 16) return -5;
     if (batch == 0) return 0;
-    if (!A) return -6;
-    if (!X) return -7;
-    if (!info) return -8;
-    if (!nsat) return -9;
+    if (!A || reinterpret_cast<uintptr_t>(A) % 16) return -6;
+    if (!X || reinterpret_cast<uintptr_t>(X) % 16) return -7;
+    if (!info || reinterpret_cast<uintptr_t>(info) % 4) return -8;
+    if (!nsat || reinterpret_cast<uintptr_t>(nsat) % 8) return -9;
     switch (n) {
 #define HPDINV_FXP(NN) case NN: return fxp::launch<NN>(method, m, f, batch, A, X, info, nsat, stream);
         HPDINV_FXP(1) HPDINV_FXP(2) HPDINV_FXP(3) HPDINV_FXP(4) HPDINV_FXP(5) HPDINV_FXP(6)
