@@ -10,7 +10,7 @@ cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"; mkdir -p gpurun_out; O=gpurun_out
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/ev_status.txt
 timeout 600 python __graft_entry__.py smoke > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/ev_status.txt
 timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo "bench default rc=$?" >> $O/ev_status.txt
-for c in ${CONFIGS:-1 3 4 5 6 7}; do
+for c in ${CONFIGS:-1 3 4 5 6 7 8}; do
   timeout 900 python bench.py --config $c --no-e2e > $O/bench_cfg$c.json 2> $O/bench_cfg$c.err; echo "bench cfg$c rc=$?" >> $O/ev_status.txt
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(reg|grp|blk|lane|generic|solve|nh|base|fxp)" -c 400 --csv --log-file $O/launches.csv \
