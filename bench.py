@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-library", action="store_true", help="skip the vendor-library comparison")
+    p.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
+                   help="replay each step from a CUDA graph (auto: for launch-bound batches, cfg1)")
     p.add_argument("--inv-method", choices=["proposed", "eqsolve", "trimat"], default="proposed",
                    help="SURVEY 8(f) f3: time one of the paper's existing methods on the GPU instead")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -233,6 +235,18 @@ def run_ours(args, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
     bad = int((info != 0).sum().item())
+    # launch-bound batches (cfg1: 1024 matrices, a few µs of GPU work) replay the step from a CUDA
+    # graph so the host-side Python/ctypes overhead does not pose as kernel time
+    use_graph = args.graph == "on" or (args.graph == "auto" and algorithmic_bytes(cfg) * B < 64 * 2**20)
+    launch = "direct C-ABI call per step"
+    if use_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        graph.replay()
+        torch.cuda.synchronize()
+        step = graph.replay
+        launch = "CUDA graph of the C-ABI call (one kernel node), replayed per step"
     barrier()
     torch.cuda.synchronize()
 
@@ -334,7 +348,7 @@ def run_ours(args, rank, world, local_rank):
                    "batch_per_gpu": B, "global_batch": world * B,
                    "elem": "complex64" if cfg.dtype == torch.complex64 else "complex128",
                    "method": cfg.method, "layout": cfg.layout,
-                   "parallelism": "batch slices, %d rank(s), no collective" % world,
+                   "parallelism": "batch slices, %d rank(s), no collective" % world, "launch": launch,
                    "l2": "inputs larger than L2 (%.0f MB working set > 126 MB); no flush"
                    % ((bj_bytes) / 1e6) if bj_bytes > L2_BYTES else "working set fits L2"},
         "roofline": roof,
