@@ -97,3 +97,28 @@ def test_gloo_world2_slices_and_timing():
         assert p.exitcode == 0
     assert t == [2.0, 10.0]
     assert torch.equal(allA, wl.generate(wl.CONFIGS[2], 0, 600))
+
+
+def test_rhs_and_fxp_generators_slice_invariant():
+    """f1 right-hand sides and f4 fixed-point inputs are chunk-keyed like the matrices: any
+    slice equals the same rows of the full draw; the quantised raws stay inside Q(m, f)."""
+    cfg6 = wl.CONFIGS[6]
+    full = wl.generate_rhs(cfg6, 0, 9000)
+    assert torch.equal(full[4000:7000], wl.generate_rhs(cfg6, 4000, 3000))
+    cfg8 = wl.CONFIGS[8]
+    A, raw = wl.generate_fxp(cfg8, 0, 300)
+    A2, raw2 = wl.generate_fxp(cfg8, 100, 50)
+    assert torch.equal(A[100:150], A2) and torch.equal(raw[100:150], raw2)
+    lim = 2 ** (cfg8.qm + cfg8.qf)
+    assert int(raw.max()) <= lim - 1 and int(raw.min()) >= -lim
+    assert torch.equal(A, A.conj().transpose(1, 2))
+    assert torch.linalg.eigvalsh(A).min() > 0
+
+
+def test_vector_layouts_roundtrip():
+    Y = wl.generate_rhs(wl.CONFIGS[6], 0, 77)
+    for layout, ld in (("aos", None), ("soa", None), ("soa", 91)):
+        store, view = wl.vec_layout(Y, layout, ld)
+        assert torch.equal(view.contiguous(), Y)
+        if layout == "soa":
+            assert view.stride() == (1, ld or 77)
