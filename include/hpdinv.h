@@ -130,6 +130,20 @@ int ldl_solve_batched_c128(int64_t batch, int n,
                            cuDoubleComplex *Xv, int64_t strideX_mat, int64_t strideX_elem,
                            int32_t *info, cudaStream_t stream);
 
+/* The batched solve from HOST buffers (end to end): the same chunked, double-buffered
+ * H2D -> kernel -> D2H pipeline as hpdinv_inv_host.  A, Y, Xv host pointers with the device
+ * entry points' layouts (strides in elements; only the upper triangle of an interleaved A
+ * crosses PCIe); d_work / work_bytes: caller-owned device workspace, 256-byte aligned, at least
+ * hpdinv_solve_host_workspace_bytes(dtype, n, chunk) (chunk is halved until it fits).
+ * Returns 0, -k for invalid argument k (1 method, 2 dtype, 3 batch, 4 n, 5/6 A, 8/9 Y,
+ * 11/12 Xv, 14 info, 15 d_work, 16 work_bytes), or a cudaError_t.  Asynchronous on `stream`. */
+size_t hpdinv_solve_host_workspace_bytes(int dtype, int n, int64_t chunk);
+int hpdinv_solve_host(int method, int dtype, int64_t batch, int n,
+                      const void *A_host, int64_t strideA_mat, int64_t strideA_elem,
+                      const void *Y_host, int64_t strideY_mat, int64_t strideY_elem,
+                      void *X_host, int64_t strideX_mat, int64_t strideX_elem, int32_t *info_host,
+                      void *d_work, size_t work_bytes, int64_t chunk, cudaStream_t stream);
+
 /* Name of the solve kernel the dispatcher would launch (static string; NULL if invalid). */
 const char *hpdinv_solve_kernel_name(int method, int dtype, int n);
 

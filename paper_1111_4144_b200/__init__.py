@@ -20,7 +20,8 @@ from ._lib import EXPORTS, HpdinvError, lib  # noqa: F401
 __all__ = [
     "chol_inv_batched_c64", "chol_inv_batched_c128", "ldl_inv_batched_c64",
     "ldl_inv_batched_c128", "chol_solve_batched_c64", "chol_solve_batched_c128",
-    "ldl_solve_batched_c64", "ldl_solve_batched_c128", "solve", "solve_kernel_name", "invert",
+    "ldl_solve_batched_c64", "ldl_solve_batched_c128", "solve", "solve_host", "solve_host_workspace_bytes",
+    "solve_kernel_name", "invert",
     "invert_method", "method_kernel_name", "nonherm_inv_batched_c64", "nonherm_inv_batched_c128",
     "invert_nonhermitian", "nonherm_kernel_name", "fxp_invert", "invert_host", "host_workspace_bytes", "kernel_name", "version", "HpdinvError",
 ]
@@ -165,6 +166,41 @@ _SOLVE = {
 def solve(A, Y, method: str = "chol", Xv=None, info=None, stream=None):
     """Batched A_b x_b = y_b with the same factorisation."""
     return _SOLVE[(method, A.dtype)](A, Y, Xv, info, stream)
+
+
+def solve_host(A_host: torch.Tensor, Y_host: torch.Tensor, method: str = "chol", X_host=None, info_host=None,
+               workspace: Optional[torch.Tensor] = None, chunk: int = 0, stream=None):
+    """hpdinv_solve_host: the batched solve from host (pinned) tensors, end to end."""
+    if A_host.is_cuda or Y_host.is_cuda:
+        raise ValueError("solve_host expects host tensors")
+    dtype = A_host.dtype
+    batch, n = A_host.shape[0], A_host.shape[1]
+    sAm, sAe = _strides(A_host)
+    sYm, sYe = _vstrides(Y_host)
+    if X_host is None:
+        X_host = torch.empty_strided(Y_host.shape, Y_host.stride(), dtype=dtype, pin_memory=True)
+    sXm, sXe = _vstrides(X_host)
+    if info_host is None:
+        info_host = torch.empty(batch, dtype=torch.int32, pin_memory=True)
+    dt = {torch.complex64: 0, torch.complex128: 1}[dtype]
+    if workspace is None:
+        ch = chunk if chunk > 0 else max(min(batch, 4096), (batch + 7) // 8)
+        workspace = torch.empty(int(lib().hpdinv_solve_host_workspace_bytes(dt, n, ch)), dtype=torch.uint8, device="cuda")
+    rc = lib().hpdinv_solve_host({"chol": 0, "ldl": 1}[method], dt, batch, n,
+                                 ctypes.c_void_p(A_host.data_ptr()), sAm, sAe,
+                                 ctypes.c_void_p(Y_host.data_ptr()), sYm, sYe,
+                                 ctypes.c_void_p(X_host.data_ptr()), sXm, sXe,
+                                 ctypes.c_void_p(info_host.data_ptr()), ctypes.c_void_p(workspace.data_ptr()),
+                                 workspace.numel(), chunk, ctypes.c_void_p(_stream_handle(stream)))
+    if rc < 0:
+        raise ValueError("hpdinv_solve_host rejected argument %d" % (-rc))
+    if rc > 0:
+        raise HpdinvError("hpdinv_solve_host: CUDA error %d" % rc)
+    return X_host, info_host
+
+
+def solve_host_workspace_bytes(dtype: torch.dtype, n: int, chunk: int) -> int:
+    return int(lib().hpdinv_solve_host_workspace_bytes({torch.complex64: 0, torch.complex128: 1}[dtype], n, chunk))
 
 
 def solve_kernel_name(method: str, dtype: torch.dtype, n: int):

@@ -47,6 +47,11 @@ def lib() -> ctypes.CDLL:
     L.hpdinv_inv_batched_method.argtypes = [I, I] + inv_args
     L.hpdinv_method_kernel_name.restype = ctypes.c_char_p
     L.hpdinv_method_kernel_name.argtypes = [I, I, I]
+    L.hpdinv_solve_host_workspace_bytes.restype = ctypes.c_size_t
+    L.hpdinv_solve_host_workspace_bytes.argtypes = [I, I, I64]
+    L.hpdinv_solve_host.restype = I
+    L.hpdinv_solve_host.argtypes = [I, I, I64, I, P, I64, I64, P, I64, I64, P, I64, I64, P, P,
+                                    ctypes.c_size_t, I64, P]
     L.hpdinv_solve_kernel_name.restype = ctypes.c_char_p
     L.hpdinv_solve_kernel_name.argtypes = [I, I, I]
     L.hpdinv_host_workspace_bytes.restype = ctypes.c_size_t
@@ -68,6 +73,7 @@ EXPORTS = (
     "ldl_inv_batched_c64", "ldl_inv_batched_c128",
     "chol_solve_batched_c64", "chol_solve_batched_c128",
     "ldl_solve_batched_c64", "ldl_solve_batched_c128", "hpdinv_solve_kernel_name",
+    "hpdinv_solve_host_workspace_bytes", "hpdinv_solve_host",
     "hpdinv_inv_batched_method", "hpdinv_method_kernel_name",
     "nonherm_inv_batched_c64", "nonherm_inv_batched_c128", "hpdinv_nonherm_kernel_name",
     "hpdinv_fxp_inv_batched",

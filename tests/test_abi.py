@@ -64,6 +64,9 @@ def test_validation_without_gpu(lib):
     assert lib.hpdinv_solve_kernel_name(0, 0, 8) == b"k_solve_reg<c64,chol>"
     assert lib.hpdinv_solve_kernel_name(1, 1, 64) == b"k_solve_gen<c128,ldl>"
     assert lib.hpdinv_solve_kernel_name(0, 0, 65) is None
+    assert lib.hpdinv_solve_host_workspace_bytes(0, 8, 1024) >= 2 * 8 * (64 + 16) * 1024
+    assert lib.hpdinv_solve_host(0, 0, 4, 8, z, 1, 4, z, 1, 4, z, 1, 4, z, z, 0, 0, z) == -5
+    assert lib.hpdinv_solve_host(2, 0, 4, 8, z, 1, 4, z, 1, 4, z, 1, 4, z, z, 0, 0, z) == -1
     # existing methods (f3): argument k of the 10-argument form is k + 2
     assert lib.hpdinv_inv_batched_method(4, 0, 4, 8, fake, 1, 4, fake, 1, 4, fake, z) == -1
     assert lib.hpdinv_inv_batched_method(2, 2, 4, 8, fake, 1, 4, fake, 1, 4, fake, z) == -2

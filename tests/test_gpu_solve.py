@@ -165,3 +165,31 @@ def test_inplace_padded_and_side_stream(orc, n):
     s.synchronize()
     assert x.data_ptr() == Yv.data_ptr()
     assert torch.equal(x.contiguous(), ref.contiguous()) and torch.equal(info, rinfo)
+
+
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+@pytest.mark.parametrize("n", [4, 8, 20])
+def test_solve_host_matches_device(n, layout):
+    """hpdinv_solve_host (chunked H2D -> kernel -> D2H from pinned host buffers) returns the
+    device solve's x and info bit for bit, including a ragged last chunk."""
+    cfg = wl.Config(92, n, torch.complex64, 0, "chol", layout, "bbh", float(n), 0.1, task="solve")
+    B = 5000
+    A = wl.generate(cfg, 0, B, device="cuda")
+    Y = wl.generate_rhs(cfg, 0, B, device="cuda")
+    A[17, 2, 2] = -50.0                                 # one flagged system
+    _, Av = wl.to_layout(A, layout)
+    _, Yv = wl.vec_layout(Y, layout)
+    xd, idv = hp.solve(Av, Yv, "chol")
+    torch.cuda.synchronize()
+    As, _ = wl.to_layout(A.cpu(), layout)
+    Ys, _ = wl.vec_layout(Y.cpu(), layout)
+    As, Ys = As.pin_memory(), Ys.pin_memory()
+    if layout == "soa":
+        Ah = wl.soa_view(As, B, n)
+        Yh = torch.as_strided(Ys, (B, n), (1, B))
+    else:
+        Ah, Yh = As, Ys
+    xh, ih = hp.solve_host(Ah, Yh, "chol", chunk=1536)
+    torch.cuda.synchronize()
+    assert torch.equal(ih, idv.cpu()) and int(ih[17]) > 0
+    assert torch.equal(torch.nan_to_num(xh.contiguous()), torch.nan_to_num(xd.cpu().contiguous()))
