@@ -313,13 +313,14 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": world * B / (te.item() / 1e3), "unit": UNIT_SOLVE, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(cfg.elem_bytes * cfg.n * B + 4 * B), "ms_per_step": te.item(),
                "chunk": chunk, "matches_device_run": bool(same), "api": "hpdinv_solve_host (pinned host buffers)"}
-    if not args.no_e2e and cfg.task == "inv" and args.inv_method == "proposed":
+    if not args.no_e2e and cfg.task in ("inv", "nonherm") and args.inv_method == "proposed":
+        nh = cfg.task == "nonherm"
         A_host = store.cpu().pin_memory()
         if cfg.layout == "soa":
             vh = wl.soa_view(A_host, B, cfg.n)
             X_host = torch.empty_like(A_host).pin_memory()
             xh = wl.soa_view(X_host, B, cfg.n)
-            h2d = cfg.elem_bytes * cfg.n * (cfg.n + 1) // 2 * B
+            h2d = cfg.elem_bytes * (cfg.n * cfg.n if nh else cfg.n * (cfg.n + 1) // 2) * B
         else:
             vh = A_host
             X_host = torch.empty_like(A_host).pin_memory()
@@ -329,8 +330,9 @@ def run_ours(args, rank, world, local_rank):
         chunk = max(4096, B // 8)
         ws = torch.empty(hp.host_workspace_bytes(cfg.dtype, cfg.n, chunk), dtype=torch.uint8, device=dev)
         e2e_steps = max(3, min(steps, 10))
+        hmethod = "nonherm" if nh else cfg.method
         for _ in range(2):
-            hp.invert_host(vh, cfg.method, xh, info_h, ws, chunk)
+            hp.invert_host(vh, hmethod, xh, info_h, ws, chunk)
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
@@ -338,7 +340,7 @@ def run_ours(args, rank, world, local_rank):
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(e2e_steps):
-            hp.invert_host(vh, cfg.method, xh, info_h, ws, chunk)
+            hp.invert_host(vh, hmethod, xh, info_h, ws, chunk)
         b.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -400,7 +402,7 @@ def run_ours(args, rank, world, local_rank):
         out["config"]["task"] = ("solve (1 right-hand side per matrix)" if solve else
                                  "non-Hermitian inversion D^-1 = D*(DD*)^-1")
         out.pop("roofline_baseline_formula", None)
-        if e2e is None and not solve:
+        if e2e is None:
             out["e2e_note"] = "no host-buffer entry point for this task yet"
         if cfg.task == "nonherm":
             out["metric"] = "non-Hermitian matrices inverted/sec (SURVEY 8(f) f2, P:135-141), 1 B200"

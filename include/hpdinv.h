@@ -215,7 +215,9 @@ int hpdinv_fxp_inv_batched(int method, int m, int f, int64_t batch, int n, const
  * into chunks of `chunk` matrices (0 = automatic) that flow through a double-buffered
  * H2D -> kernel -> D2H pipeline on two internal copy streams plus `stream` for the kernels.
  * Only the upper triangle is copied host->device for an interleaved (SoA) host A.
- *   method: 0 Cholesky, 1 LDL.  dtype: 0 complex64, 1 complex128.
+ *   method: 0 Cholesky, 1 LDL, 2 the non-Hermitian inversion of nonherm_inv_batched_* (all n^2
+ *   entries of A are copied; half a slot each for input and output).  dtype: 0 complex64,
+ *   1 complex128.
  *   A_host / X_host / info_host: host pointers, same addressing and layout classes as the
  *   device entry points (strides in elements).  X_host may not alias A_host.
  *   d_work / work_bytes: caller-owned device workspace, 256-byte aligned, at least

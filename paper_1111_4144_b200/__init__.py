@@ -305,7 +305,7 @@ def invert_host(A_host: torch.Tensor, method: str = "chol", X_host=None, info_ho
     if workspace is None:
         ch = chunk if chunk > 0 else max(min(batch, 4096), (batch + 7) // 8)
         workspace = torch.empty(host_workspace_bytes(dtype, n, ch), dtype=torch.uint8, device="cuda")
-    rc = lib().hpdinv_inv_host({"chol": 0, "ldl": 1}[method], {torch.complex64: 0, torch.complex128: 1}[dtype],
+    rc = lib().hpdinv_inv_host({"chol": 0, "ldl": 1, "nonherm": 2}[method], {torch.complex64: 0, torch.complex128: 1}[dtype],
                                batch, n, ctypes.c_void_p(A_host.data_ptr()), sAm, sAe,
                                ctypes.c_void_p(X_host.data_ptr()), sXm, sXe,
                                ctypes.c_void_p(info_host.data_ptr()), ctypes.c_void_p(workspace.data_ptr()),

@@ -22,14 +22,17 @@ inline int64_t slot_bytes(int n, size_t elem, int64_t chunk) {
     return b + (chunk * 4 + 255) / 256 * 256;
 }
 
+// method 0 Cholesky, 1 LDL (in place), 2 non-Hermitian (out of place into `out`)
 int launch_inv(int method, int dtype, int64_t m, int n, void* buf, int64_t sm, int64_t se,
-               int32_t* info, cudaStream_t s) {
+               int32_t* info, cudaStream_t s, void* out = nullptr) {
     if (dtype == 0) {
         auto* p = static_cast<cuFloatComplex*>(buf);
+        if (method == 2) return nonherm_inv_batched_c64(m, n, p, sm, se, static_cast<cuFloatComplex*>(out), sm, se, info, s);
         return method ? ldl_inv_batched_c64(m, n, p, sm, se, p, sm, se, info, s)
                       : chol_inv_batched_c64(m, n, p, sm, se, p, sm, se, info, s);
     }
     auto* p = static_cast<cuDoubleComplex*>(buf);
+    if (method == 2) return nonherm_inv_batched_c128(m, n, p, sm, se, static_cast<cuDoubleComplex*>(out), sm, se, info, s);
     return method ? ldl_inv_batched_c128(m, n, p, sm, se, p, sm, se, info, s)
                   : chol_inv_batched_c128(m, n, p, sm, se, p, sm, se, info, s);
 }
@@ -190,7 +193,7 @@ int hpdinv_inv_host(int method, int dtype, int64_t batch, int n,
                     const void* A_host, int64_t sAm, int64_t sAe,
                     void* X_host, int64_t sXm, int64_t sXe, int32_t* info_host,
                     void* d_work, size_t work_bytes, int64_t chunk, cudaStream_t stream) {
-    if (method < 0 || method > 1) return -1;
+    if (method < 0 || method > 2) return -1;
     if (dtype < 0 || dtype > 1) return -2;
     if (batch < 0) return -3;
     if (n < 1 || n > HPDINV_MAX_N) return -4;
@@ -213,10 +216,14 @@ int hpdinv_inv_host(int method, int dtype, int64_t batch, int n,
     if (reinterpret_cast<uintptr_t>(d_work) % 256) return -12;
 
     const int64_t sb = slot_bytes(n, elem, chunk);
+    // method 2 (non-Hermitian) is out of place: half a slot in, half out, chunk / 2 per step
+    const bool nh = method == 2;
+    const int64_t cbuf = chunk;
+    if (nh) chunk = std::max<int64_t>(1, chunk / 2);
     Slot slot[2];
     for (int s = 0; s < 2; s++) {
         slot[s].buf = static_cast<char*>(d_work) + s * sb;
-        slot[s].info = reinterpret_cast<int32_t*>(slot[s].buf + (int64_t(n) * n * chunk * int64_t(elem) + 255) / 256 * 256);
+        slot[s].info = reinterpret_cast<int32_t*>(slot[s].buf + (int64_t(n) * n * cbuf * int64_t(elem) + 255) / 256 * 256);
     }
 
     cudaStream_t h2d = nullptr, d2h = nullptr;
@@ -247,7 +254,11 @@ int hpdinv_inv_host(int method, int dtype, int64_t batch, int n,
         const int64_t m = std::min(chunk, batch - b0);
         if (c >= 2) chk(cudaStreamWaitEvent(h2d, ev_out[s], 0));   // slot s drained
         // ---- H2D: device slot is interleaved (ld = chunk) when the host A is, else AoS
-        if (a_soa) {
+        char* res = nh ? slot[s].buf + int64_t(n) * n * chunk * int64_t(elem) : slot[s].buf;
+        if (a_soa && nh) {                  // non-Hermitian: every plane of D
+            chk(cudaMemcpy2DAsync(slot[s].buf, chunk * elem, A + b0 * elem, sAe * elem, m * elem, int64_t(n) * n,
+                                  cudaMemcpyHostToDevice, h2d));
+        } else if (a_soa) {
             for (int i = 0; i < n; i++) {   // planes (i, i..n-1): only the upper triangle
                 const char* src = A + (b0 + int64_t(i * n + i) * sAe) * elem;
                 char* dst = slot[s].buf + int64_t(i * n + i) * chunk * elem;
@@ -262,24 +273,24 @@ int hpdinv_inv_host(int method, int dtype, int64_t batch, int n,
         // ---- kernel, in place on the slot
         chk(cudaStreamWaitEvent(stream, ev_in[s], 0));
         if (e == cudaSuccess) {
-            rc = a_soa ? launch_inv(method, dtype, m, n, slot[s].buf, 1, chunk, slot[s].info, stream)
-                       : launch_inv(method, dtype, m, n, slot[s].buf, int64_t(n) * n, 1, slot[s].info, stream);
+            rc = a_soa ? launch_inv(method, dtype, m, n, slot[s].buf, 1, chunk, slot[s].info, stream, res)
+                       : launch_inv(method, dtype, m, n, slot[s].buf, int64_t(n) * n, 1, slot[s].info, stream, res);
         }
         chk(cudaEventRecord(ev_done[s], stream));
         // ---- D2H into the caller's layout
         chk(cudaStreamWaitEvent(d2h, ev_done[s], 0));
         const int64_t dsm = a_soa ? 1 : int64_t(n) * n, dse = a_soa ? chunk : 1;
         if (x_soa && a_soa) {
-            chk(cudaMemcpy2DAsync(X + b0 * elem, sXe * elem, slot[s].buf, chunk * elem, m * elem,
+            chk(cudaMemcpy2DAsync(X + b0 * elem, sXe * elem, res, chunk * elem, m * elem,
                                   int64_t(n) * n, cudaMemcpyDeviceToHost, d2h));
         } else if (x_aos && !a_soa) {
-            chk(cudaMemcpy2DAsync(X + b0 * sXm * elem, sXm * elem, slot[s].buf, int64_t(n) * n * elem,
+            chk(cudaMemcpy2DAsync(X + b0 * sXm * elem, sXm * elem, res, int64_t(n) * n * elem,
                                   int64_t(n) * n * elem, m, cudaMemcpyDeviceToHost, d2h));
         } else {
             // mixed layouts: element-plane / matrix scatter with 2-D copies (one per element)
             for (int64_t el = 0; el < int64_t(n) * n; el++)
                 chk(cudaMemcpy2DAsync(X + (b0 * sXm + el * sXe) * elem, sXm * elem,
-                                      slot[s].buf + el * dse * elem, dsm * elem, elem, m,
+                                      res + el * dse * elem, dsm * elem, elem, m,
                                       cudaMemcpyDeviceToHost, d2h));
         }
         chk(cudaMemcpyAsync(info_host + b0, slot[s].info, m * 4, cudaMemcpyDeviceToHost, d2h));

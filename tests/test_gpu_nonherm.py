@@ -107,3 +107,23 @@ def test_padded_layouts_match(orc):
     Y2, i2 = hp.invert_nonhermitian(Dv)
     torch.cuda.synchronize()
     assert torch.equal(Y1, Y2.contiguous()) and torch.equal(i1, i2)
+
+
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+def test_host_pipeline_matches_device(layout):
+    """hpdinv_inv_host(method 2) -- D from pinned host memory, chunked -- equals the device call."""
+    cfg = wl.CONFIGS[7]
+    B = 3000
+    D = wl.generate(cfg, 0, B, device="cuda")
+    _, Dv = wl.to_layout(D, layout)
+    Yd, idv = hp.invert_nonhermitian(Dv)
+    torch.cuda.synchronize()
+    store, _ = wl.to_layout(D.cpu(), layout)
+    store = store.pin_memory()
+    Dh = wl.soa_view(store, B, cfg.n) if layout == "soa" else store
+    Xh = torch.empty_like(store).pin_memory()
+    xh = wl.soa_view(Xh, B, cfg.n) if layout == "soa" else Xh
+    xh, ih = hp.invert_host(Dh, "nonherm", xh, chunk=1024)
+    torch.cuda.synchronize()
+    assert torch.equal(ih, idv.cpu())
+    assert torch.equal(xh.contiguous(), Yd.cpu().contiguous())
