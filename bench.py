@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-library", action="store_true", help="skip the vendor-library comparison")
+    p.add_argument("--batch", type=int, default=None,
+                   help="override the config's per-GPU batch (e.g. an L2-resident study; not a BASELINE line)")
     p.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                    help="replay each step from a CUDA graph (auto: for launch-bound batches, cfg1)")
     p.add_argument("--inv-method", choices=["proposed", "eqsolve", "trimat"], default="proposed",
@@ -184,6 +186,9 @@ def run_ours(args, rank, world, local_rank):
     import paper_1111_4144_b200 as hp
 
     cfg = wl.CONFIGS[args.config]
+    if args.batch:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, batch=int(args.batch))
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     B = cfg.batch
