@@ -4,12 +4,17 @@
 One step = one pass of the whole hot path (load upper(A) -> Cholesky/LDL -> proposed
 inversion -> mirror -> store) over one batch of synthetic matrices, i.e.
 one call of the C ABI entry point.  Default workload: BASELINE.json configs[1] (cfg2: 2^20
-complex64 8x8 HPD matrices, interleaved layout) on N=1 GPU.  `--config k` selects another.
+complex64 8x8 HPD matrices, interleaved layout); the same line carries `per_config` entries
+for the other metric sizes (cfg3 N=16, cfg4 N=64, cfg5 N=32 LDL), each timed the same way.
+`--config k` makes another workload the headline.
 
-Multi-GPU (torchrun, one process per GPU): every rank inverts its own slice of a global
-batch of N x B matrices generated locally from chunk-keyed seeds (weak scaling, no data-path
-collective).  Timing: CUDA events on the launching stream between a barrier +
-synchronize on both sides; the max over ranks is reported.
+Multi-GPU: `--gpus N` without a torchrun environment re-launches this script
+under `torch.distributed.run` with N ranks (one per GPU, NCCL, 127.0.0.1).  Default scaling
+is STRONG: the fixed BASELINE global batch B is sharded, rank r owning the contiguous slice
+`workloads.shard(r, W, B)` and generating it on its own device from the chunk-keyed seeds;
+`--scaling weak` gives every rank a full B instead.  No collective touches the data path:
+NCCL carries only the start barrier and the max-over-ranks reduction of the timings.
+value = global matrices / max_r (rank r's device time per step).
 
 `--impl reference` times the fp64 CPU oracle (the reference arm of this tier) on bounded
 samples of the same workload, on rank 0 only.
@@ -17,9 +22,12 @@ samples of the same workload, on rank 0 only.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -34,36 +42,39 @@ from paper_1111_4144_b200 import workloads as wl  # noqa: E402
 
 METRIC = "HPD matrices inverted/sec (N=8,16,64) and % of HBM/FP roofline, 1-8 B200"
 UNIT = "matrices/s"
+METRIC_SOLVE = "HPD linear systems solved/sec (SURVEY 8(f) f1: A x = y, eqs. 5-7 / 12-14), 1 B200"
+UNIT_SOLVE = "systems/s"
 L2_BYTES = 126 * 2**20
 SMS = 148
+DEFAULT_PER_CONFIG = {2: "3,4,5"}      # the headline cfg2 line also times the other metric sizes
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=None)
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", type=int, default=2, choices=sorted(wl.CONFIGS))
+    p.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                   help="strong: shard the fixed global batch over the ranks (default); weak: a full batch per rank")
+    p.add_argument("--per-config", default=None,
+                   help="comma list of extra configs timed into `per_config` ('' = none; default 3,4,5 for cfg2)")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-library", action="store_true", help="skip the vendor-library comparison")
     p.add_argument("--batch", type=int, default=None,
-                   help="override the config's per-GPU batch (e.g. an L2-resident study; not a BASELINE line)")
+                   help="override the headline config's global batch (e.g. an L2-resident study; not a BASELINE line)")
     p.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
-                   help="replay each step from a CUDA graph (auto: for launch-bound batches, cfg1)")
+                   help="replay each step from a CUDA graph (auto: for launch-bound per-rank batches)")
     p.add_argument("--inv-method", choices=["proposed", "eqsolve", "trimat"], default="proposed",
                    help="SURVEY 8(f) f3: time one of the paper's existing methods on the GPU instead")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
-    return p.parse_args()
+    return p.parse_args(argv)
 
 
 # ----------------------------------------------------------------------------- helpers
-METRIC_SOLVE = "HPD linear systems solved/sec (SURVEY 8(f) f1: A x = y, eqs. 5-7 / 12-14), 1 B200"
-UNIT_SOLVE = "systems/s"
-
-
 def algorithmic_bytes(cfg: wl.Config) -> int:
     """Per matrix: read the upper triangle, write all n^2 entries of X and one int32 info
     (solve: read the upper triangle and y, write x and info)."""
@@ -94,7 +105,9 @@ def peaks():
 
 
 def fp_peak_tflops(dtype: torch.dtype, mhz: float) -> float:
-    """FP32 / FP64 FMA peak from unit counts: 148 SMs x {128, 64} FMA/clk x 2."""
+    """FP32 / FP64 FMA peak from unit counts: 148 SMs x {128, 64} FMA/clk x 2.
+    (FP64: the DMMA tensor path measured 37.05 TF/s, `profiles/r02_mma_peaks.txt`, on the same
+    FP64 datapath as DFMA -- the derived 37.2 is the larger, so it is the denominator.)"""
     lanes = 128 if dtype == torch.complex64 else 64
     return SMS * lanes * 2 * mhz * 1e6 / 1e12
 
@@ -168,123 +181,265 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def load_traffic(cfg: wl.Config, kernel: str):
+class NullSampler:
+    def start(self):
+        pass
+
+    def stop(self):
+        pass
+
+    def summary(self):
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "note": "no GPU"}
+
+
+def load_traffic(cfg: wl.Config, kernel: str, batch: int):
     """Per-launch DRAM bytes of this kernel from the committed ncu --set full summary."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         t = json.load(open(path))
         rec = t.get("cfg%d" % cfg.cid)
-        if rec and rec.get("kernel") == kernel and rec.get("batch") == cfg.batch:
+        if rec and rec.get("kernel") == kernel and rec.get("batch") == batch:
             return float(rec["dram_bytes_per_launch"])
     except Exception:
         pass
     return None
 
 
-# ------------------------------------------------------------------------------ ours
-def run_ours(args, rank, world, local_rank):
-    import paper_1111_4144_b200 as hp
+# ------------------------------------------------------------- multi-rank plumbing
+class Dist:
+    """Barrier and max/min reductions over the ranks (NCCL on the GPU box, gloo in the CPU
+    test); a no-op for one rank.  Nothing here touches the data path."""
 
-    cfg = wl.CONFIGS[args.config]
-    if args.batch:
-        import dataclasses
-        cfg = dataclasses.replace(cfg, batch=int(args.batch))
-    dev = torch.device("cuda", local_rank)
-    torch.cuda.set_device(dev)
-    B = cfg.batch
-    if cfg.task == "fxp":
-        return run_fxp(args, cfg, rank, world, dev)
-    A = wl.generate(cfg, rank * B, B, device=dev, seed=args.seed)   # this rank's slice
-    store, view = wl.to_layout(A, cfg.layout)
-    del A
-    info = torch.empty(B, dtype=torch.int32, device=dev)
-    solve = cfg.task == "solve"
-    metric, unit = (METRIC_SOLVE, UNIT_SOLVE) if solve else (METRIC, UNIT)
-    if solve:
-        Y = wl.generate_rhs(cfg, rank * B, B, device=dev, seed=args.seed)
-        ystore, yview = wl.vec_layout(Y, cfg.layout)
-        del Y
-        Xv = torch.empty_strided(yview.shape, yview.stride(), dtype=cfg.dtype, device=dev)
-        kernel = hp.solve_kernel_name(cfg.method, cfg.dtype, cfg.n)
+    def __init__(self, world: int, device):
+        self.world = world
+        self.device = device
 
-        def step():
-            hp.solve(view, yview, cfg.method, Xv=Xv, info=info)
-    elif cfg.task == "nonherm":
-        X = wl.empty_like_layout(view)
-        kernel = hp.nonherm_kernel_name(cfg.dtype, cfg.n)
+    def barrier(self):
+        if self.world > 1:
+            if self.device.type == "cuda":
+                torch.distributed.barrier(device_ids=[self.device.index])
+            else:
+                torch.distributed.barrier()
 
-        def step():
-            hp.invert_nonhermitian(view, Dinv=X, info=info)
-    elif args.inv_method != "proposed":
-        X = wl.empty_like_layout(view)
-        kernel = hp.method_kernel_name(args.inv_method, cfg.dtype, cfg.n)
+    def _reduce(self, vals, op):
+        t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=self.device)
+        if self.world > 1:
+            torch.distributed.all_reduce(t, op=op)
+        return t.tolist()
 
-        def step():
-            hp.invert_method(view, args.inv_method, X=X, info=info)
-    else:
-        X = wl.empty_like_layout(view)
-        kernel = hp.kernel_name(cfg.method, cfg.dtype, B, cfg.n, (view.stride(0), view.stride(2)))
+    def max(self, vals):
+        return self._reduce(vals, torch.distributed.ReduceOp.MAX if self.world > 1 else None)
 
-        def step():
-            hp.invert(view, cfg.method, X=X, info=info)
+    def min(self, vals):
+        return self._reduce(vals, torch.distributed.ReduceOp.MIN if self.world > 1 else None)
 
-    per_step_guess = algorithmic_bytes(cfg) * B / 6.0e12
-    steps = args.steps if args.steps is not None else max(20, min(2000, int(0.5 / per_step_guess)))
-    warmup = max(3, args.warmup)
 
-    def barrier():
-        if world > 1:
-            torch.distributed.barrier(device_ids=[local_rank])
+def shard_plan(cfg: wl.Config, rank: int, world: int, scaling: str, batch=None):
+    """(start, count, global_batch) of this rank.  strong: the fixed global batch B is split
+    into contiguous slices ([r B/W, (r+1) B/W)); weak: rank r owns the r-th
+    full batch of a global batch of W x B."""
+    B = int(batch) if batch else cfg.batch
+    if scaling == "weak":
+        return rank * B, B, world * B
+    start, count = wl.shard(rank, world, B)
+    return start, count, B
 
-    for _ in range(warmup):
-        step()
-    torch.cuda.synchronize()
-    bad = int((info != 0).sum().item())
-    # launch-bound batches (cfg1: 1024 matrices, a few µs of GPU work) replay the step from a CUDA
-    # graph so the host-side Python/ctypes overhead does not pose as kernel time
-    use_graph = args.graph == "on" or (args.graph == "auto" and algorithmic_bytes(cfg) * B < 64 * 2**20)
-    launch = "direct C-ABI call per step"
-    if use_graph:
+
+class CudaBackend:
+    """The product path: inputs generated on this rank's GPU, one C-ABI call per step, CUDA
+    events on the launching stream."""
+
+    def __init__(self, device):
+        import paper_1111_4144_b200 as hp
+        self.hp = hp
+        self.device = device
+
+    def sync(self):
+        torch.cuda.synchronize(self.device)
+
+    def event(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(torch.cuda.current_stream(self.device))
+        return e
+
+    @staticmethod
+    def elapsed_ms(a, b):
+        return a.elapsed_time(b)
+
+    def sampler(self):
+        return ClockSampler(self.device.index)
+
+    def prepare(self, cfg: wl.Config, start: int, count: int, args):
+        hp = self.hp
+        dev = self.device
+        st = {"cfg": cfg, "count": count}
+        A = wl.generate(cfg, start, count, device=dev, seed=args.seed)
+        store, view = wl.to_layout(A, cfg.layout)
+        del A
+        st.update(store=store, view=view)
+        info = torch.empty(count, dtype=torch.int32, device=dev)
+        st["info"] = info
+        if cfg.task == "solve":
+            Y = wl.generate_rhs(cfg, start, count, device=dev, seed=args.seed)
+            ystore, yview = wl.vec_layout(Y, cfg.layout)
+            del Y
+            Xv = torch.empty_strided(yview.shape, yview.stride(), dtype=cfg.dtype, device=dev)
+            st.update(ystore=ystore, yview=yview, X=Xv, kernel=hp.solve_kernel_name(cfg.method, cfg.dtype, cfg.n))
+            st["step"] = lambda: hp.solve(view, yview, cfg.method, Xv=Xv, info=info)
+        elif cfg.task == "nonherm":
+            X = wl.empty_like_layout(view)
+            st.update(X=X, kernel=hp.nonherm_kernel_name(cfg.dtype, cfg.n))
+            st["step"] = lambda: hp.invert_nonhermitian(view, Dinv=X, info=info)
+        elif args.inv_method != "proposed":
+            X = wl.empty_like_layout(view)
+            st.update(X=X, kernel=hp.method_kernel_name(args.inv_method, cfg.dtype, cfg.n))
+            st["step"] = lambda: hp.invert_method(view, args.inv_method, X=X, info=info)
+        else:
+            X = wl.empty_like_layout(view)
+            st.update(X=X, kernel=hp.kernel_name(cfg.method, cfg.dtype, count, cfg.n,
+                                                 (view.stride(0), view.stride(2)), (X.stride(0), X.stride(2))))
+            st["step"] = lambda: hp.invert(view, cfg.method, X=X, info=info)
+        return st
+
+    def maybe_graph(self, st, per_step_s: float, mode: str):
+        """Launch-bound per-rank batches (cfg1, or any slice whose kernel is a few tens of µs)
+        replay the step from a CUDA graph so the host-side Python/ctypes overhead does not pose
+        as kernel time."""
+        use = mode == "on" or (mode == "auto" and per_step_s < 60e-6)
+        if not use:
+            return st["step"], "direct C-ABI call per step"
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            step()
+            st["step"]()
         graph.replay()
-        torch.cuda.synchronize()
-        step = graph.replay
-        launch = "CUDA graph of the C-ABI call (one kernel node), replayed per step"
-    barrier()
-    torch.cuda.synchronize()
+        self.sync()
+        st["graph"] = graph
+        return graph.replay, "CUDA graph of the C-ABI call (one kernel node), replayed per step"
 
-    sampler = ClockSampler(torch.cuda.current_device())
-    stream = torch.cuda.current_stream()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    sampler.start()
-    t0.record(stream)
-    for k in range(steps):
-        evs[k][0].record(stream)
+    def nonzero_info(self, st):
+        return int((st["info"] != 0).sum().item())
+
+    def release(self):
+        torch.cuda.empty_cache()
+
+
+def timed_loop(step, steps: int, warmup: int, backend, dist: Dist):
+    """W untimed warm-up steps, then exactly `steps` timed steps between a barrier +
+    synchronize on both sides.  Returns (ms_per_step, kernel_ms, wall_span_ms) reduced over
+    the ranks: the max of the per-rank device times; the wall span is the host-clock interval
+    from the earliest rank's start to the latest rank's end (ranks share one host clock)."""
+    for _ in range(warmup):
         step()
-        evs[k][1].record(stream)
-    t1.record(stream)
-    torch.cuda.synchronize()
-    sampler.stop()
-    barrier()
-    elapsed_ms = t0.elapsed_time(t1)
-    kern_ms = sum(a.elapsed_time(b) for a, b in evs) / steps
-    t = torch.tensor([elapsed_ms, kern_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    elapsed_ms, kern_ms = t.tolist()
-    ms_per_step = elapsed_ms / steps
-    value = world * B / (ms_per_step / 1e3)
+    backend.sync()
+    dist.barrier()
+    backend.sync()
+    t_host0 = time.time()
+    t0 = backend.event()
+    evs = []
+    for _ in range(steps):
+        a = backend.event()
+        step()
+        evs.append((a, backend.event()))
+    t1 = backend.event()
+    backend.sync()
+    t_host1 = time.time()
+    dist.barrier()
+    elapsed = backend.elapsed_ms(t0, t1)
+    kern = sum(backend.elapsed_ms(a, b) for a, b in evs) / steps
+    elapsed, kern, t_end = dist.max([elapsed, kern, t_host1])
+    (t_start,) = dist.min([t_host0])
+    return elapsed / steps, kern, (t_end - t_start) * 1e3
 
-    # ---- end to end through the host-buffer C entry point (H2D + kernel + D2H timed)
-    e2e = None
-    if not args.no_e2e and solve:
-        # the solve end to end through hpdinv_solve_host (pinned host A, y -> x)
+
+def roofline(cfg: wl.Config, count: int, kern_ms: float, kernel: str):
+    """Roofline of the (single) kernel of the step on this rank's slice: algorithmic bytes (or
+    the paper's multiply count for the FP-bound sizes) per launch / the kernel's event time."""
+    pk = peaks()
+    bytes_launch = algorithmic_bytes(cfg) * count
+    mem_s = bytes_launch / (pk["hbm_gbs"] * 1e9)
+    fp_tf = fp_peak_tflops(cfg.dtype, pk["sm_max_mhz"])
+    flops_launch = 8.0 * cmul_per_matrix(cfg.n, cfg.task) * count
+    fp_s = flops_launch / (fp_tf * 1e12)
+    if fp_s > mem_s:
+        achieved = flops_launch / (kern_ms / 1e3) / 1e12
+        tc = kernel.startswith("k_dmma")
+        roof = {"bound": "tensor" if tc else "alu", "achieved": achieved, "peak": fp_tf, "unit": "TFLOP/s",
+                "frac": achieved / fp_tf,
+                "peak_source": "derived FP%d peak: 148 SMs x %d FMA/clk x 2 x %.0f MHz%s"
+                % (32 if cfg.dtype == torch.complex64 else 64, 128 if cfg.dtype == torch.complex64 else 64,
+                   pk["sm_max_mhz"], " (FP64 DMMA tensor path; measured DMMA peak 37.05 TF/s, "
+                   "profiles/r02_mma_peaks.txt)" if tc else "")}
+    else:
+        achieved = bytes_launch / (kern_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "peak_source": pk["source"]}
+    roof["traffic"] = load_traffic(cfg, kernel, count)
+    roof["algorithmic_bytes_per_launch"] = bytes_launch
+    roof["flops_per_launch"] = flops_launch
+    roof["kernel"] = kernel
+    roof["kernel_ms"] = kern_ms
+    # BASELINE.json's own formula: max(16 N^2 batch / HBM, multiply count / FP peak)
+    bj_bytes = 2 * cfg.elem_bytes * cfg.n ** 2 * count
+    bj_t = max(bj_bytes / (pk["hbm_gbs"] * 1e9), fp_s)
+    return roof, {"time_s": bj_t, "frac": bj_t / (kern_ms / 1e3), "bytes": bj_bytes,
+                  "note": "BASELINE.json north_star formula"}
+
+
+def config_dict(cfg: wl.Config, world: int, scaling: str, batch=None):
+    """The workload description shared by both arms (so the driver sees the same config)."""
+    B = int(batch) if batch else cfg.batch
+    global_batch = B * world if scaling == "weak" else B
+    bj_bytes = 2 * cfg.elem_bytes * cfg.n ** 2 * global_batch
+    return {"workload": "cfg%d: %s" % (cfg.cid, cfg.desc), "n": cfg.n, "global_batch": global_batch,
+            "elem": "complex64" if cfg.dtype == torch.complex64 else "complex128",
+            "method": cfg.method, "layout": cfg.layout,
+            "parallelism": "batch sharded over %d rank(s) (%s scaling), no collective" % (world, scaling),
+            "l2": ("inputs larger than L2 (%.0f MB > 126 MB); no flush" % (bj_bytes / 1e6)
+                   if bj_bytes > L2_BYTES else "working set fits L2")}
+
+
+def run_config(args, cfg: wl.Config, rank: int, world: int, dist: Dist, backend, steps=None, batch=None):
+    """One workload on this rank: generate the rank's slice, time the step, reduce over the
+    ranks.  Returns (summary dict, state) -- the state keeps the buffers for e2e and checks."""
+    start, count, global_batch = shard_plan(cfg, rank, world, args.scaling, batch)
+    st = backend.prepare(cfg, start, count, args)
+    per_step_guess = max(algorithmic_bytes(cfg) * count / 6.0e12,
+                         8.0 * cmul_per_matrix(cfg.n, cfg.task) * count / 3.0e13, 2e-6)
+    if steps is None:
+        steps = max(20, min(2000, int(0.5 / per_step_guess)))
+    warmup = max(3, args.warmup)
+    step, launch = backend.maybe_graph(st, per_step_guess, args.graph)
+    sampler = backend.sampler()
+    # the warm-up and the timed steps both live inside timed_loop; the sampler runs over it
+    sampler.start()
+    ms_per_step, kern_ms, wall_ms = timed_loop(step, steps, warmup, backend, dist)
+    sampler.stop()
+    bad = backend.nonzero_info(st)
+    (bad,) = dist.max([bad])
+    roof, bj = roofline(cfg, count, kern_ms, st["kernel"])
+    out = {
+        "value": global_batch / (ms_per_step / 1e3), "unit": UNIT_SOLVE if cfg.task == "solve" else UNIT,
+        "ms_per_step": ms_per_step, "kernel_ms": kern_ms, "wall_span_ms": wall_ms, "steps": steps,
+        "warmup": warmup, "n_gpus": world, "global_batch": global_batch, "batch_per_rank": count,
+        "rank_slice": [start, start + count], "launch": launch, "roofline": roof, "roofline_baseline_formula": bj,
+        "clocks": sampler.summary(), "gpu_launches": steps, "info_nonzero": int(bad),
+    }
+    return out, st
+
+
+def e2e_measure(args, cfg: wl.Config, st, world: int, dist: Dist, dev, steps: int):
+    """The same metric end to end through the host-buffer C entry points (pinned host A [, y]
+    -> H2D -> kernel -> D2H of X and info), timed with CUDA events; the result read back must
+    match the device-resident run bit for bit."""
+    hp = CudaBackend(dev).hp
+    B = st["count"]
+    store = st["store"]
+    stream = torch.cuda.current_stream(dev)
+    e2e_steps = max(3, min(steps, 10))
+    chunk = max(4096, B // 8)
+    if cfg.task == "solve":
         A_host = store.cpu().pin_memory()
-        Y_host = ystore.cpu().pin_memory()
+        Y_host = st["ystore"].cpu().pin_memory()
         if cfg.layout == "soa":
             vh = wl.soa_view(A_host, B, cfg.n)
             yh = torch.as_strided(Y_host, (B, cfg.n), (1, Y_host.shape[1]))
@@ -295,111 +450,76 @@ def run_ours(args, rank, world, local_rank):
         X_host = torch.empty_like(Y_host).pin_memory()
         xh = torch.as_strided(X_host, yh.shape, yh.stride())
         info_h = torch.empty(B, dtype=torch.int32).pin_memory()
-        chunk = max(4096, B // 8)
         ws = torch.empty(hp.solve_host_workspace_bytes(cfg.dtype, cfg.n, chunk), dtype=torch.uint8, device=dev)
-        e2e_steps = max(3, min(steps, 10))
-        for _ in range(2):
+
+        def call():
             hp.solve_host(vh, yh, cfg.method, xh, info_h, ws, chunk)
-        torch.cuda.synchronize()
-        barrier()
-        torch.cuda.synchronize()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(e2e_steps):
-            hp.solve_host(vh, yh, cfg.method, xh, info_h, ws, chunk)
-        b.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        te = torch.tensor([a.elapsed_time(b) / e2e_steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-        same = torch.equal(xh.contiguous(), Xv.cpu().contiguous()) and torch.equal(info_h, info.cpu())
-        e2e = {"value": world * B / (te.item() / 1e3), "unit": UNIT_SOLVE, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(cfg.elem_bytes * cfg.n * B + 4 * B), "ms_per_step": te.item(),
-               "chunk": chunk, "matches_device_run": bool(same), "api": "hpdinv_solve_host (pinned host buffers)"}
-    if not args.no_e2e and cfg.task in ("inv", "nonherm") and args.inv_method == "proposed":
+        d2h = cfg.elem_bytes * cfg.n * B + 4 * B
+        unit, api = UNIT_SOLVE, "hpdinv_solve_host (pinned host buffers)"
+    else:
         nh = cfg.task == "nonherm"
         A_host = store.cpu().pin_memory()
+        X_host = torch.empty_like(A_host).pin_memory()
         if cfg.layout == "soa":
             vh = wl.soa_view(A_host, B, cfg.n)
-            X_host = torch.empty_like(A_host).pin_memory()
             xh = wl.soa_view(X_host, B, cfg.n)
             h2d = cfg.elem_bytes * (cfg.n * cfg.n if nh else cfg.n * (cfg.n + 1) // 2) * B
         else:
-            vh = A_host
-            X_host = torch.empty_like(A_host).pin_memory()
-            xh = X_host
+            vh, xh = A_host, X_host
             h2d = cfg.elem_bytes * cfg.n * cfg.n * B
         info_h = torch.empty(B, dtype=torch.int32).pin_memory()
-        chunk = max(4096, B // 8)
         ws = torch.empty(hp.host_workspace_bytes(cfg.dtype, cfg.n, chunk), dtype=torch.uint8, device=dev)
-        e2e_steps = max(3, min(steps, 10))
         hmethod = "nonherm" if nh else cfg.method
-        for _ in range(2):
-            hp.invert_host(vh, hmethod, xh, info_h, ws, chunk)
-        torch.cuda.synchronize()
-        barrier()
-        torch.cuda.synchronize()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(e2e_steps):
-            hp.invert_host(vh, hmethod, xh, info_h, ws, chunk)
-        b.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        te = torch.tensor([a.elapsed_time(b) / e2e_steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-        # the result read back must match the device-resident run bit for bit
-        same = torch.equal(xh.contiguous(), X.cpu().contiguous()) and torch.equal(info_h, info.cpu())
-        e2e = {"value": world * B / (te.item() / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(cfg.elem_bytes * cfg.n * cfg.n * B + 4 * B),
-               "ms_per_step": te.item(), "chunk": chunk, "matches_device_run": bool(same),
-               "api": "hpdinv_inv_host (pinned host buffers)"}
 
-    # ---- roofline of the (single) kernel of the step
-    pk = peaks()
-    clocks = sampler.summary()
-    bytes_launch = algorithmic_bytes(cfg) * B
-    mem_s = bytes_launch / (pk["hbm_gbs"] * 1e9)
-    fp_tf = fp_peak_tflops(cfg.dtype, pk["sm_max_mhz"])
-    flops_launch = 8.0 * cmul_per_matrix(cfg.n, cfg.task) * B
-    fp_s = flops_launch / (fp_tf * 1e12)
-    if fp_s > mem_s:
-        achieved = flops_launch / (kern_ms / 1e3) / 1e12
-        roof = {"bound": "alu", "achieved": achieved, "peak": fp_tf, "unit": "TFLOP/s",
-                "frac": achieved / fp_tf, "peak_source": "derived: 148 SMs x %d FMA/clk x 2 x %.0f MHz"
-                % (128 if cfg.dtype == torch.complex64 else 64, pk["sm_max_mhz"])}
-    else:
-        achieved = bytes_launch / (kern_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"], "peak_source": pk["source"]}
-    roof["traffic"] = load_traffic(cfg, kernel)
-    roof["algorithmic_bytes_per_launch"] = bytes_launch
-    roof["kernel"] = kernel
-    roof["kernel_ms"] = kern_ms
-    # BASELINE.json's own formula: max(16 N^2 batch / HBM, multiply count / FP peak)
-    bj_bytes = 2 * cfg.elem_bytes * cfg.n ** 2 * B
-    bj_t = max(bj_bytes / (pk["hbm_gbs"] * 1e9), fp_s)
+        def call():
+            hp.invert_host(vh, hmethod, xh, info_h, ws, chunk)
+        d2h = cfg.elem_bytes * cfg.n * cfg.n * B + 4 * B
+        unit, api = UNIT, "hpdinv_inv_host (pinned host buffers)"
+    for _ in range(2):
+        call()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(e2e_steps):
+        call()
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    (ms,) = dist.max([a.elapsed_time(b) / e2e_steps])
+    same = torch.equal(xh.contiguous(), st["X"].cpu().contiguous()) and torch.equal(info_h, st["info"].cpu())
+    global_batch = B * world if args.scaling == "weak" else cfg.batch
+    return {"value": global_batch / (ms / 1e3), "unit": unit, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": ms, "chunk": chunk,
+            "matches_device_run": bool(same), "api": api}
+
+
+def run_rank(args, rank, world, dist: Dist, backend, extras=None):
+    """The rank function of the product run (device agnostic through `backend`): the headline
+    workload, then the other metric sizes (`per_config`), each sharded, timed and reduced over
+    the ranks in the same way.  `extras(cfg, st, head)` adds keys that need the headline's
+    buffers (e2e, the library comparison) before they are freed."""
+    cfg = wl.CONFIGS[args.config]
+    head, st = run_config(args, cfg, rank, world, dist, backend, steps=args.steps, batch=args.batch)
+    solve = cfg.task == "solve"
+    more = extras(cfg, st, head) if extras is not None else {}
+    del st
+    backend.release()
     out = {
-        "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": steps,
-        "warmup": warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32" if cfg.dtype == torch.complex64 else "f64",
+        "metric": METRIC_SOLVE if solve else METRIC, "value": head["value"], "unit": head["unit"],
+        "n_gpus": world, "steps": head["steps"], "warmup": head["warmup"], "ms_per_step": head["ms_per_step"],
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "f32" if cfg.dtype == torch.complex64 else "f64",
         "data": "synthetic (seeded, chunk-keyed; BASELINE.json configs recipe)",
-        "config": {"workload": "cfg%d: %s" % (cfg.cid, cfg.desc), "n": cfg.n,
-                   "batch_per_gpu": B, "global_batch": world * B,
-                   "elem": "complex64" if cfg.dtype == torch.complex64 else "complex128",
-                   "method": cfg.method, "layout": cfg.layout,
-                   "parallelism": "batch slices, %d rank(s), no collective" % world, "launch": launch,
-                   "l2": "inputs larger than L2 (%.0f MB working set > 126 MB); no flush"
-                   % ((bj_bytes) / 1e6) if bj_bytes > L2_BYTES else "working set fits L2"},
-        "roofline": roof,
-        "roofline_baseline_formula": {"time_s": bj_t, "frac": bj_t / (kern_ms / 1e3),
-                                      "bytes": bj_bytes, "note": "BASELINE.json north_star formula"},
-        "clocks": clocks, "gpu_launches": steps, "info_nonzero": bad, "e2e": e2e,
+        "config": config_dict(cfg, world, args.scaling, args.batch),
+        "roofline": head["roofline"], "roofline_baseline_formula": head["roofline_baseline_formula"],
+        "clocks": head["clocks"], "gpu_launches": head["gpu_launches"], "info_nonzero": head["info_nonzero"],
+        "e2e": None, "launch": head["launch"], "wall_span_ms": head["wall_span_ms"],
+        "batch_per_rank": head["batch_per_rank"], "kernel_ms": head["kernel_ms"],
     }
+    out.update(more)
     if args.inv_method != "proposed":
         out["config"]["inv_method"] = args.inv_method + " (SURVEY 8(f) f3: the paper's existing method, not the product path)"
         out.pop("roofline_baseline_formula")
@@ -407,12 +527,47 @@ def run_ours(args, rank, world, local_rank):
         out["config"]["task"] = ("solve (1 right-hand side per matrix)" if solve else
                                  "non-Hermitian inversion D^-1 = D*(DD*)^-1")
         out.pop("roofline_baseline_formula", None)
-        if e2e is None:
-            out["e2e_note"] = "no host-buffer entry point for this task yet"
         if cfg.task == "nonherm":
             out["metric"] = "non-Hermitian matrices inverted/sec (SURVEY 8(f) f2, P:135-141), 1 B200"
-    if rank == 0 and world == 1 and not args.no_library:
-        out["library_baseline"] = library_baseline(cfg, view, yview if solve else None, dev)
+    # ---- the other metric sizes, each timed the same way on the same ranks
+    extra = args.per_config if args.per_config is not None else DEFAULT_PER_CONFIG.get(args.config, "")
+    if args.batch is None and args.inv_method == "proposed":
+        per = {}
+        for tok in [t for t in extra.split(",") if t.strip()]:
+            c = wl.CONFIGS[int(tok)]
+            res, st = run_config(args, c, rank, world, dist, backend,
+                                 steps=min(args.steps, 50) if args.steps else None)
+            del st
+            backend.release()
+            res["workload"] = config_dict(c, world, args.scaling)["workload"]
+            res["dtype"] = "f32" if c.dtype == torch.complex64 else "f64"
+            per["cfg%d" % c.cid] = res
+        if per:
+            out["per_config"] = per
+            out["gpu_launches"] += sum(r["gpu_launches"] for r in per.values())
+            out["gpu_launches_note"] = "headline steps + per_config steps (one kernel launch per step)"
+    return out
+
+
+def run_ours(args, rank, world, local_rank):
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist = Dist(world, dev)
+    backend = CudaBackend(dev)
+    cfg = wl.CONFIGS[args.config]
+    if cfg.task == "fxp":
+        return run_fxp(args, cfg, rank, world, dev)
+
+    def extras(cfg, st, head):
+        more = {}
+        if not args.no_e2e and (cfg.task == "solve" or (cfg.task in ("inv", "nonherm")
+                                                         and args.inv_method == "proposed")):
+            more["e2e"] = e2e_measure(args, cfg, st, world, dist, dev, head["steps"])
+        if rank == 0 and world == 1 and not args.no_library:
+            more["library_baseline"] = library_baseline(cfg, st["view"], st.get("yview"), dev)
+        return more
+
+    out = run_rank(args, rank, world, dist, backend, extras)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, args, budget_s=args.cpu_seconds, dev=dev)
     return out
@@ -424,31 +579,20 @@ def run_fxp(args, cfg, rank, world, dev):
     the cfg8 batch, and reports the study itself: mean relative error of the three methods vs
     the double-precision inverse on a sample of the GPU results (Fig. 1)."""
     import paper_1111_4144_b200 as hp
-    B = cfg.batch
-    A, raw = wl.generate_fxp(cfg, rank * B, B, device=dev, seed=args.seed)
+    start, B, global_batch = shard_plan(cfg, rank, world, args.scaling)
+    A, raw = wl.generate_fxp(cfg, start, B, device=dev, seed=args.seed)
     X = torch.empty_like(raw)
     info = torch.empty(B, dtype=torch.int32, device=dev)
     nsat = torch.empty(B, dtype=torch.int64, device=dev)
     steps = args.steps if args.steps is not None else 10
     warmup = max(3, args.warmup)
-    for _ in range(warmup):
-        hp.fxp_invert(raw, cfg.qm, cfg.qf, "proposed", X, info, nsat)
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier(device_ids=[dev.index])
+    dist = Dist(world, dev)
+    backend = CudaBackend(dev)
     sampler = ClockSampler(torch.cuda.current_device())
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler.start()
-    a.record()
-    for _ in range(steps):
-        hp.fxp_invert(raw, cfg.qm, cfg.qf, "proposed", X, info, nsat)
-    b.record()
-    torch.cuda.synchronize()
+    ms, _, _ = timed_loop(lambda: hp.fxp_invert(raw, cfg.qm, cfg.qf, "proposed", X, info, nsat),
+                          steps, warmup, backend, dist)
     sampler.stop()
-    t = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms = t.item()
     # the study on a sample (host double-precision reference)
     S = min(B, 4096)
     Xr = np.linalg.inv(A[:S].cpu().numpy())
@@ -469,13 +613,11 @@ def run_fxp(args, cfg, rank, world, dev):
     achieved = byts / (ms / 1e3) / 1e9
     out = {
         "metric": "fixed-point Q%d.%d emulated inversions/sec (SURVEY 8(f) f4, P:206-208), 1 B200" % (cfg.qm, cfg.qf),
-        "value": world * B / (ms / 1e3), "unit": "matrices/s", "n_gpus": world, "steps": steps,
-        "warmup": warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "value": global_batch / (ms / 1e3), "unit": "matrices/s", "n_gpus": world, "steps": steps,
+        "warmup": warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "int64 (Q%d.%d raws, 128-bit products)" % (cfg.qm, cfg.qf),
         "data": "synthetic (SPEC.md ensemble, seeded, chunk-keyed)",
-        "config": {"workload": "cfg%d: %s" % (cfg.cid, cfg.desc), "n": cfg.n, "batch_per_gpu": B,
-                   "task": "fxp", "format": "Q%d.%d" % (cfg.qm, cfg.qf),
-                   "l2": "inputs larger than L2" if byts > L2_BYTES else "working set fits L2"},
+        "config": dict(config_dict(cfg, world, args.scaling), task="fxp", format="Q%d.%d" % (cfg.qm, cfg.qf)),
         "roofline": {"bound": "alu", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "kernel": "k_fxp<%d>" % cfg.n, "kernel_ms": ms,
                      "traffic": None, "note": "integer emulation (128-bit software products and "
@@ -553,16 +695,16 @@ def oracle_sample(cfg: wl.Config, count: int, seed: int, dev):
     return A.cpu().to(torch.complex128).numpy()
 
 
-def oracle_run(cfg: wl.Config, Ah, yh):
+def oracle_run(cfg: wl.Config, Ah, yh, nthreads: int = 0):
     import oracle
     if cfg.task == "fxp":
-        X, info, _ = oracle.fxp_inv_batched(Ah, cfg.qm, cfg.qf, "proposed")
+        X, info, _ = oracle.fxp_inv_batched(Ah, cfg.qm, cfg.qf, "proposed", nthreads=nthreads)
         return X, info
     if cfg.task == "nonherm":
-        return oracle.nonherm_batched(Ah)
+        return oracle.nonherm_batched(Ah, nthreads=nthreads)
     if cfg.task == "solve":
-        return oracle.solve_batched(Ah, yh, cfg.method)
-    return oracle.inv_batched(Ah, cfg.method)
+        return oracle.solve_batched(Ah, yh, cfg.method, nthreads=nthreads)
+    return oracle.inv_batched(Ah, cfg.method, nthreads=nthreads)
 
 
 def oracle_rhs(cfg: wl.Config, count: int, seed: int, dev):
@@ -572,6 +714,8 @@ def oracle_rhs(cfg: wl.Config, count: int, seed: int, dev):
 
 
 def cpu_baseline(cfg: wl.Config, args, budget_s: float, dev):
+    """The oracle as it stands on the box's host cores (all threads, then 1 thread), on a
+    bounded sample of the same workload."""
     import oracle
     oracle.build()
     cores = oracle.max_threads()
@@ -585,9 +729,15 @@ def cpu_baseline(cfg: wl.Config, args, budget_s: float, dev):
     t0 = time.perf_counter()
     oracle_run(cfg, Ah, yh)
     dt = time.perf_counter() - t0
+    # 1 thread on a sample of ~budget/4 seconds
+    c1 = int(max(16, min(count, budget_s / 4.0 / max(per * cores, 1e-9))))
+    t1 = time.perf_counter()
+    oracle_run(cfg, Ah[:c1], None if yh is None else yh[:c1], nthreads=1)
+    dt1 = time.perf_counter() - t1
     return {"value": count / dt, "unit": UNIT_SOLVE if cfg.task == "solve" else UNIT, "cores": cores, "kind": "oracle",
             "sample": "first %d of the %d matrices of cfg%d (%s), fp64 C oracle, OpenMP over matrices"
             % (count, cfg.batch, cfg.cid, cfg.method), "seconds": dt,
+            "one_thread": {"value": c1 / dt1, "cores": 1, "sample": "first %d matrices" % c1, "seconds": dt1},
             "cpu": _cpu_model()}
 
 
@@ -630,12 +780,11 @@ def run_reference(args, rank, world):
     solve = cfg.task == "solve"
     UNITX = UNIT_SOLVE if solve else UNIT
     return {
-        "impl": "reference", "metric": METRIC_SOLVE if solve else METRIC, "value": value, "unit": UNITX, "n_gpus": world,
-        "steps": steps, "warmup": warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg%d: %s" % (cfg.cid, cfg.desc), "n": cfg.n,
-                   "batch_per_gpu": cfg.batch, "method": cfg.method, "layout": cfg.layout,
-                   "sample_per_step": count},
+        "impl": "reference", "metric": METRIC_SOLVE if solve else METRIC, "value": value, "unit": UNITX,
+        "n_gpus": world, "steps": steps, "warmup": warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, chunk-keyed; BASELINE.json configs recipe)",
+        "config": config_dict(cfg, world, args.scaling, args.batch),
+        "sample_per_step": count,
         "cpu_baseline": {"value": value, "unit": UNITX, "cores": cores, "kind": "oracle",
                          "sample": "first %d of the %d matrices of cfg%d per step" % (count, cfg.batch, cfg.cid),
                          "cpu": _cpu_model()},
@@ -644,8 +793,29 @@ def run_reference(args, rank, world):
     }
 
 
-def main():
-    args = parse()
+# ------------------------------------------------------------------- launcher
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(nproc: int, argv) -> int:
+    """Re-launch this script under torch.distributed.run with one rank per GPU (the driver's
+    own launch line); returns the launcher's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(nproc),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.abspath(__file__)] + list(argv)
+    return subprocess.call(cmd)
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        return spawn_ranks(args.gpus, argv)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -654,6 +824,9 @@ def main():
             return 0
         print(json.dumps(run_reference(args, rank, world)), flush=True)
         return 0
+    if world != args.gpus:
+        print("bench.py: --gpus %d but WORLD_SIZE=%d" % (args.gpus, world), file=sys.stderr)
+        return 2
     if world > 1:
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))

@@ -37,6 +37,24 @@ def _strides(t: torch.Tensor) -> Tuple[int, int]:
     return s0, s2
 
 
+_WORKSPACES = {}
+
+
+def _auto_workspace(nbytes: int) -> torch.Tensor:
+    """Device workspace for the host entry points when the caller passes none.  It is kept
+    (per device, grown on demand) rather than freed on return: the copies the call enqueued on
+    the library's internal streams still use it, and those streams are invisible to PyTorch's
+    caching allocator."""
+    dev = torch.cuda.current_device()
+    ws = _WORKSPACES.get(dev)
+    if ws is None or ws.numel() < nbytes:
+        if ws is not None:
+            torch.cuda.synchronize(dev)          # the old buffer may still be in flight
+        ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        _WORKSPACES[dev] = ws
+    return ws
+
+
 def _stream_handle(stream: Optional[torch.cuda.Stream]) -> int:
     s = stream if stream is not None else torch.cuda.current_stream()
     return int(s.cuda_stream)
@@ -185,7 +203,7 @@ def solve_host(A_host: torch.Tensor, Y_host: torch.Tensor, method: str = "chol",
     dt = {torch.complex64: 0, torch.complex128: 1}[dtype]
     if workspace is None:
         ch = chunk if chunk > 0 else max(min(batch, 4096), (batch + 7) // 8)
-        workspace = torch.empty(int(lib().hpdinv_solve_host_workspace_bytes(dt, n, ch)), dtype=torch.uint8, device="cuda")
+        workspace = _auto_workspace(int(lib().hpdinv_solve_host_workspace_bytes(dt, n, ch)))
     rc = lib().hpdinv_solve_host({"chol": 0, "ldl": 1}[method], dt, batch, n,
                                  ctypes.c_void_p(A_host.data_ptr()), sAm, sAe,
                                  ctypes.c_void_p(Y_host.data_ptr()), sYm, sYe,
@@ -304,7 +322,7 @@ def invert_host(A_host: torch.Tensor, method: str = "chol", X_host=None, info_ho
         info_host = torch.empty(batch, dtype=torch.int32, pin_memory=True)
     if workspace is None:
         ch = chunk if chunk > 0 else max(min(batch, 4096), (batch + 7) // 8)
-        workspace = torch.empty(host_workspace_bytes(dtype, n, ch), dtype=torch.uint8, device="cuda")
+        workspace = _auto_workspace(host_workspace_bytes(dtype, n, ch))
     rc = lib().hpdinv_inv_host({"chol": 0, "ldl": 1, "nonherm": 2}[method], {torch.complex64: 0, torch.complex128: 1}[dtype],
                                batch, n, ctypes.c_void_p(A_host.data_ptr()), sAm, sAe,
                                ctypes.c_void_p(X_host.data_ptr()), sXm, sXe,

@@ -92,6 +92,11 @@ int run(int dtype, bool ldl, const LaunchArgs& c) {
     if (v <= 0) return v;
     int rc = kNoKernel;
     const bool soa = classify(c.batch, c.n, c.sAm, c.sAe) == kSoA && classify(c.batch, c.n, c.sXm, c.sXe) == kSoA;
+    // complex128 n = 64 Cholesky with a contiguous A: the FP64 tensor-core kernel (k_dmma)
+    if (dmma_accepts(dtype, ldl, c.n, c.sAm, c.sAe)) {
+        rc = launch_dmma(c);
+        if (rc != kNoKernel) return rc;
+    }
     switch (family(dtype, c.n, soa)) {
         case kReg: rc = launch_reg(dtype, ldl, c); break;
         case kGrp: rc = launch_grp(dtype, ldl, c); break;
@@ -230,7 +235,11 @@ const char* hpdinv_kernel_name(int method, int dtype, int64_t batch, int n, int6
     if (classify(batch, n, sAm, sAe) == kInvalid || classify(batch, n, sXm, sXe) == kInvalid)
         return nullptr;
     const bool soa = classify(batch, n, sAm, sAe) == kSoA && classify(batch, n, sXm, sXe) == kSoA;
-    return family_name(family(dtype, n, soa), dtype, method != 0);
+    Family f = family(dtype, n, soa);
+    // the same decision launch_grp takes (it declines plane strides >= 4 GiB -> k_lane)
+    if (f == kGrp && !grp_strides_ok(sAe, sXe, dtype == 0 ? 8 : 16)) f = n <= lane_max_n(dtype) ? kLane : kGeneric;
+    if (classify(batch, n, sAm, sAe) == kAoS && dmma_accepts(dtype, method != 0, n, sAm, sAe)) return "k_dmma<c128,chol>";
+    return family_name(f, dtype, method != 0);
 }
 
 const char* hpdinv_version(void) { return "hpdinv 0.2.0 (sm_100a)"; }

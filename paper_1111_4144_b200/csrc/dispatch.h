@@ -40,6 +40,8 @@ int launch_lane(int dtype, bool ldl, const LaunchArgs& a);      // k_lane_c64.cu
 int launch_generic(int dtype, bool ldl, const LaunchArgs& a);   // k_generic.cu
 int launch_grp(int dtype, bool ldl, const LaunchArgs& a);       // k_grp.cu (interleaved, c64 9..16)
 int launch_blk(int dtype, bool ldl, const LaunchArgs& a);       // k_blk.cu (n = 32, 64)
+int launch_dmma(const LaunchArgs& a);                            // k_dmma.cu (c128, n = 64, Cholesky, AoS A)
+bool dmma_accepts(int dtype, bool ldl, int n, int64_t sAm, int64_t sAe);
 int launch_solve(int dtype, bool ldl, const SolveArgs& a);      // k_solve.cu (any n <= 64)
 const char* solve_kernel_name(int dtype, bool ldl, int n);
 int launch_base(int method, int dtype, const LaunchArgs& a);    // k_base.cu (methods 2, 3)
@@ -51,6 +53,12 @@ const char* nh_kernel_name(int dtype, int n);
 constexpr int reg_max_n(int dtype) { return dtype == 0 ? 8 : 6; }
 constexpr int lane_max_n(int dtype) { return dtype == 0 ? 32 : 16; }
 constexpr int grp_max_n(int dtype) { return dtype == 0 ? 16 : 0; }
+
+// k_grp addresses element planes with 32-bit byte offsets: it takes SoA plane strides below 4 GiB
+// (the launcher declines otherwise and the dispatcher falls back to k_lane)
+constexpr bool grp_strides_ok(int64_t sAe, int64_t sXe, size_t elem) {
+    return uint64_t(sAe) * elem < (uint64_t(1) << 32) && uint64_t(sXe) * elem < (uint64_t(1) << 32);
+}
 
 // Raise the dynamic shared-memory limit of `fn` on the current device once (thread-safe).
 cudaError_t ensure_smem(const void* fn, size_t bytes);

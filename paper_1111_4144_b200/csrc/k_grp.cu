@@ -29,8 +29,7 @@ static int launch_grp_t(const LaunchArgs& a) {
 #undef HPDINV_GRP
     // plane strides in bytes must fit the kernel's 32-bit address offsets (any SoA array with
     // n >= 9 that fits in device memory does)
-    const uint64_t lim = uint64_t(1) << 32;
-    if (uint64_t(a.sAe) * sizeof(cplx<T>) >= lim || uint64_t(a.sXe) * sizeof(cplx<T>) >= lim) fn = nullptr;
+    if (!grp_strides_ok(a.sAe, a.sXe, sizeof(cplx<T>))) fn = nullptr;
     if (!fn) return kNoKernel;
     cudaError_t e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
     if (e != cudaSuccess) return int(e);

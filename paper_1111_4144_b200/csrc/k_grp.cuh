@@ -256,22 +256,20 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
     // ------------------------------------------------------------------ S5: mirror + store
     if (valid) {
         // (storing each row as soon as it is final, inside S4, measured slower: 4.5 vs 4.1 ms cfg3)
+        // every entry (m, j) is written once, by the owner of column j; a flagged matrix is
+        // NaN-filled in the same store
         char* Xrow = reinterpret_cast<char*>(X + b * sXm + q * sXe);   // element (m, q + G s)
         const uint32_t seX = uint32_t(sXe * int64_t(sizeof(V)));
+        const T nan = qnan<T>();
 #pragma unroll
         for (int s = 0; s < C; s++) {
             const int j = q + G * s;
             if (j < N) {
 #pragma unroll
                 for (int m = 0; m < N; m++)
-                    grp::st(reinterpret_cast<V*>(Xrow + uint64_t(uint32_t(m * N + G * s)) * seX), col[s][m]);
+                    grp::st(reinterpret_cast<V*>(Xrow + uint64_t(uint32_t(m * N + G * s)) * seX),
+                            inf ? mk<T>(nan, nan) : col[s][m]);
             }
-        }
-        if (inf) {          // a flagged matrix is overwritten (same thread, program order)
-            const T nan = qnan<T>();
-            V* Xb = X + b * sXm;
-#pragma unroll 1
-            for (int e = q; e < N * N; e += G) Xb[int64_t(e) * sXe] = mk<T>(nan, nan);
         }
         if (q == 0) info[b] = inf;
     }

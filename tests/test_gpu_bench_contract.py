@@ -26,8 +26,17 @@ def test_default_line():
               "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
               "clocks", "gpu_launches"):
         assert k in d, k
-    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] >= 3 and d["gpu_launches"] == 5
-    assert d["config"]["workload"].startswith("cfg2")
+    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] >= 3
+    assert d["config"]["workload"].startswith("cfg2") and d["scaling"] == "strong"
+    # the other metric sizes, timed the same way (N=16, N=64, N=32 LDL)
+    per = d["per_config"]
+    assert set(per) == {"cfg3", "cfg4", "cfg5"}
+    for k, r in per.items():
+        assert r["workload"].startswith(k) and r["n_gpus"] == 1 and r["steps"] == 5
+        assert r["value"] > 0 and r["kernel_ms"] > 0 and r["info_nonzero"] == 0
+        assert 0 < r["roofline"]["frac"] <= 1.5 and "sm_mhz" in r["clocks"]
+        assert r["global_batch"] == r["batch_per_rank"]
+    assert d["gpu_launches"] == 5 + sum(r["gpu_launches"] for r in per.values())
     r = d["roofline"]
     assert r["bound"] in ("hbm", "tensor", "alu") and r["unit"] in ("GB/s", "TFLOP/s")
     assert 0 < r["frac"] <= 1.5 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
@@ -43,5 +52,8 @@ def test_default_line():
 def test_reference_arm():
     d = _run("--impl", "reference", "--steps", "1", "--warmup", "0")
     assert d["impl"] == "reference" and d["value"] > 0
+    ours = _run("--steps", "3", "--warmup", "3", "--per-config", "", "--no-e2e", "--no-library",
+                "--no-cpu-baseline")
+    assert d["config"] == ours["config"]          # the driver compares the two arms' configs
     assert d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
