@@ -54,7 +54,13 @@ int launch_dmma(const LaunchArgs& a) {
                                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return b0 == 0 ? kNoKernel : int(cudaErrorInvalidValue);
-        k_dmma<<<unsigned(nb), dm::NT, dm::SMEM, a.stream>>>(tm, nb, X, a.sXm, a.sXe, a.info + b0);
+        // persistent: one CTA of WPB warps per SM (WPB matrices in flight per SM)
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t need = (nb + dm::WPB - 1) / dm::WPB;
+        const unsigned grid = unsigned(need < sms ? need : sms);
+        k_dmma<<<grid, dm::NT, dm::SMEM, a.stream>>>(tm, nb, X, a.sXm, a.sXe, a.info + b0);
         if ((e = cudaGetLastError()) != cudaSuccess) return int(e);
     }
     return 0;
