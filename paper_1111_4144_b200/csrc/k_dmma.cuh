@@ -49,7 +49,7 @@ constexpr int NTL = 8;                               // tiles per dimension
 constexpr int NTILE = NTL * (NTL + 1) / 2;           // 36 upper tiles
 constexpr int WPB = 6;                               // warps (matrices) per CTA, one CTA per SM
 constexpr int NT = 32 * WPB;
-constexpr int TILES_B = (NTILE + 1) * 1024;          // 36 tiles + 1 scratch tile per warp
+constexpr int TILES_B = NTILE * 1024;                // 36 tiles per warp
 constexpr int AUX_B = 64 * 8 + 8 * 8;                // per warp: 1/r_kk (64 doubles), 8 mbarriers
 constexpr int SMEM = WPB * (TILES_B + AUX_B) + 1024; // + alignment slack (TMA 128B swizzle)
 
@@ -136,7 +136,137 @@ __device__ __forceinline__ void load_row(double2* Tw, const CUtensorMap* tm, int
     for (int J = I; J < NTL; J++) tma_load_tile(Tw + 64 * tidx(I, J), tm, 16 * J, 8 * I, int(b), bar);
 }
 
+#ifdef HPDINV_DMMA_PROF
+__device__ unsigned long long g_prof[16];   // per-phase cycles of lane 0, summed over warps
+#define DM_PHASE(id)                                  \
+    do {                                              \
+        if (lane == 0) {                              \
+            const long long t_ = clock64();           \
+            prof_[prof_cur_] += t_ - prof_t_;         \
+            prof_t_ = t_;                             \
+            prof_cur_ = (id);                         \
+        }                                             \
+    } while (0)
+#else
+#define DM_PHASE(id) do {} while (0)
+#endif
+
 }  // namespace dm
+
+// ---- the GEMM-shaped part of a panel with every index compile-time (one instantiation per
+// panel K): no branch between the MMAs of different tiles, immediate shared-memory offsets,
+// and the fragment loads free to be hoisted above the MMAs they feed.  (Predicated-off MMAs
+// measured to cost pipe time, and a runtime tile count puts a branch around every tile.)
+struct DmLane { int oa0, oa1, ob0, ob1, r, q; };
+using dm::CAcc;
+
+// F1 of the off-diagonal tiles + F2b:  R_KJ = E (A_KJ - sum_{P<K} R_PK^H R_PJ), J = K+1..7;
+// E (the accumulator layout of F2a) is the A operand of F2b straight from registers
+template <int K>
+__device__ __forceinline__ void dm_factor_off(double2* __restrict__ Tw, const DmLane& L, const CAcc& e) {
+    using namespace dm;
+    constexpr int NT_ = NTL - 1 - K;
+    CAcc a[NT_ > 0 ? NT_ : 1];
+#pragma unroll
+    for (int u = 0; u < NT_; u++) acc_load(a[u], Tw + 64 * tidx(K, K + 1 + u), L.oa0, L.oa1);
+#pragma unroll
+    for (int P = 0; P < K; P++) {
+#pragma unroll
+        for (int s = 0; s < 2; s++) {
+            const int ob = s ? L.ob1 : L.ob0;
+            const double2 w = Tw[64 * tidx(P, K) + ob];                  // A = -conj(R_PK)^T
+            const double ar = negd(w.x), ai = w.y, nai = negd(w.y);
+#pragma unroll
+            for (int u = 0; u < NT_; u++) {
+                const double2 v = Tw[64 * tidx(P, K + 1 + u) + ob];      // B = R_PJ
+                cmma(a[u], ar, ai, nai, v.x, v.y);
+            }
+        }
+    }
+    // A' through its own tile, read back as the B operand of E A'
+#pragma unroll
+    for (int u = 0; u < NT_; u++) acc_store(a[u], Tw + 64 * tidx(K, K + 1 + u), L.oa0, L.oa1);
+    __syncwarp();
+    double2 b0[NT_ > 0 ? NT_ : 1], b1[NT_ > 0 ? NT_ : 1];
+#pragma unroll
+    for (int u = 0; u < NT_; u++) {
+        b0[u] = Tw[64 * tidx(K, K + 1 + u) + L.ob0];
+        b1[u] = Tw[64 * tidx(K, K + 1 + u) + L.ob1];
+    }
+    __syncwarp();
+    const double ne0 = negd(e.i0), ne1 = negd(e.i1);
+#pragma unroll
+    for (int u = 0; u < NT_; u++) {
+        czero(a[u]);
+        cmma(a[u], e.r0, e.i0, ne0, b0[u].x, b0[u].y);
+        cmma(a[u], e.r1, e.i1, ne1, b1[u].x, b1[u].y);
+        acc_store(a[u], Tw + 64 * tidx(K, K + 1 + u), L.oa0, L.oa1);
+    }
+}
+
+// I1 + I2 + I3 of panel K < 7: C_KJ = sum_{M in T} R_KM X~_MJ (X~_MJ = X_JM^H for M > J),
+// X_KJ = -R_KK^-1 C_KJ (R_KK^-1 = E^H: the diagonal tile's lower half read transposed),
+// v = sum_J R_KJ X_KJ^H; C goes through its own tile to be read back as B, each lane keeping
+// its R_KJ fragments (its own slots) for I3
+template <int K>
+__device__ __forceinline__ void dm_invert_off(double2* Tw, const DmLane& L, CAcc& v) {
+    using namespace dm;
+    constexpr int NT_ = NTL - 1 - K;
+    constexpr int M0 = K + 1;
+    CAcc a[NT_];
+#pragma unroll
+    for (int u = 0; u < NT_; u++) czero(a[u]);
+#pragma unroll
+    for (int m = 0; m < NT_; m++) {
+#pragma unroll
+        for (int s = 0; s < 2; s++) {
+            const double2 w = Tw[64 * tidx(K, M0 + m) + (s ? L.oa1 : L.oa0)];   // A = R_KM
+            const double nwi = negd(w.y);
+#pragma unroll
+            for (int u = 0; u < NT_; u++) {
+                double2 x;
+                if (m <= u) x = Tw[64 * tidx(M0 + m, M0 + u) + (s ? L.ob1 : L.ob0)];
+                else { x = Tw[64 * tidx(M0 + u, M0 + m) + (s ? L.oa1 : L.oa0)]; x.y = negd(x.y); }
+                cmma(a[u], w.x, w.y, nwi, x.x, x.y);
+            }
+        }
+    }
+    const double2* tKK = Tw + 64 * tidx(K, K);
+    double ra0, ia0, ra1, ia1;                                          // A = -R_KK^-1
+    {
+        const double2 w0 = tKK[L.ob0], w1 = tKK[L.ob1];                 // E(2q+s, r)
+        const bool v0 = 2 * L.q >= L.r, v1 = 2 * L.q + 1 >= L.r;
+        ra0 = v0 ? negd(w0.x) : 0.0; ia0 = v0 ? w0.y : 0.0;
+        ra1 = v1 ? negd(w1.x) : 0.0; ia1 = v1 ? w1.y : 0.0;
+    }
+    double2 u0[NT_], u1[NT_];
+#pragma unroll
+    for (int u = 0; u < NT_; u++) {
+        double2* tKJ = Tw + 64 * tidx(K, K + 1 + u);
+        u0[u] = tKJ[L.oa0];                                             // R_KJ (own slots)
+        u1[u] = tKJ[L.oa1];
+        acc_store(a[u], tKJ, L.oa0, L.oa1);                             // C_KJ
+    }
+    __syncwarp();
+    CAcc v2;
+    czero(v2);
+    const double nia0 = negd(ia0), nia1 = negd(ia1);
+#pragma unroll
+    for (int u = 0; u < NT_; u++) {
+        const double2* tKJ = Tw + 64 * tidx(K, K + 1 + u);
+        const double2 b0 = tKJ[L.ob0], b1 = tKJ[L.ob1];
+        czero(a[u]);
+        cmma(a[u], ra0, ia0, nia0, b0.x, b0.y);
+        cmma(a[u], ra1, ia1, nia1, b1.x, b1.y);
+        CAcc& vv = (u & 1) ? v2 : v;
+        cmma(vv, u0[u].x, u0[u].y, negd(u0[u].y), a[u].r0, negd(a[u].i0));
+        cmma(vv, u1[u].x, u1[u].y, negd(u1[u].y), a[u].r1, negd(a[u].i1));
+    }
+    __syncwarp();                                                       // every B read is done
+#pragma unroll
+    for (int u = 0; u < NT_; u++) acc_store(a[u], Tw + 64 * tidx(K, K + 1 + u), L.oa0, L.oa1);
+    if (NT_ > 1) { v.r0 += v2.r0; v.r1 += v2.r1; v.i0 += v2.i0; v.i1 += v2.i1; }
+}
 
 // tmA: 3-D tensor map over A viewed as doubles {2n (re/im of a row), n rows, batch}, box
 // {16, 8, 1} (one 8 x 8 complex tile), 128-byte swizzle.  X: any layout (element (i, j) of
@@ -152,7 +282,6 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, int64_t batch, double2* X, int64
     double2* Tw = reinterpret_cast<double2*>(smem_raw + pad + warp * TILES_B);      // this warp's tiles
     double* invs = reinterpret_cast<double*>(smem_raw + pad + WPB * TILES_B + warp * AUX_B);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + pad + WPB * TILES_B + warp * AUX_B + 64 * 8);
-    double2* Ws = Tw + 64 * NTILE;                                                  // scratch tile
 #define TILE(I, J) (Tw + rowbase(I) + 64 * (J))
 
     const int r = lane >> 2, q = lane & 3;             // accumulator row, column pair
@@ -160,9 +289,15 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, int64_t batch, double2* X, int64
     // ob[s] = (2q+s, r) (B as stored / A transposed)
     const int oa0 = sw(r, 2 * q), oa1 = sw(r, 2 * q + 1);
     const int ob0 = sw(2 * q, r), ob1 = sw(2 * q + 1, r);
+    const DmLane L{oa0, oa1, ob0, ob1, r, q};
 
     const int64_t stride = int64_t(gridDim.x) * WPB;
     int64_t b = int64_t(blockIdx.x) * WPB + warp;
+#ifdef HPDINV_DMMA_PROF
+    long long prof_[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // wait F1d F2a F2b I1 I23 I4 S5 - -
+    long long prof_t_ = clock64();
+    int prof_cur_ = 8;
+#endif
     if (lane == 0) {
         for (int I = 0; I < NTL; I++) mbar_init(&bar[I], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -178,39 +313,51 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, int64_t batch, double2* X, int64
         // ========================================================== factorisation, panels up
 #pragma unroll 1
         for (int K = 0; K < NTL; K++) {
+            DM_PHASE(0);
             mbar_wait(&bar[K], par);                       // tile row K of A has landed
+            DM_PHASE(1);
             double2* tKK = TILE(K, K);
             // ---- F1 on the diagonal tile: A_KK -= sum_{P<K} R_PK^H R_PK
-            CAcc d;
+            CAcc d, d2;
             acc_load(d, tKK, oa0, oa1);
+            czero(d2);
 #pragma unroll 1
             for (int P = 0; P < K; P++) {
                 const double2* tPK = TILE(P, K);
 #pragma unroll
                 for (int s = 0; s < 2; s++) {
                     const double2 u = tPK[s ? ob1 : ob0];                 // A = -conj(R_PK)^T, B = R_PK
-                    cmma(d, negd(u.x), u.y, negd(u.y), u.x, u.y);
+                    cmma((P & 1) ? d2 : d, negd(u.x), u.y, negd(u.y), u.x, u.y);
                 }
             }
+            d.r0 += d2.r0; d.r1 += d2.r1; d.i0 += d2.i0; d.i1 += d2.i1;
+            DM_PHASE(2);
             // ---- F2a: R_KK by the right-looking recursion of eqs. 3-4 on the accumulators, and
             //      E = R_KK^-H (the same row operations applied to I), for the panel solves.
-            //      Step i broadcasts the unscaled row i and the pivot together; every lane scales
-            //      by 1/r_ii itself (the update uses conj(a_ir) a_ij / t_i = conj(r_ir) r_ij).
+            //      Step i broadcasts the unscaled rows i of A' and of E through the diagonal tile
+            //      (scratch until F2a ends: A' row i in tile row i, E row i in tile row i+4 mod 8,
+            //      so consecutive steps never touch the same row); every lane scales by 1/r_ii
+            //      itself (the update uses conj(a_ir) a_ij / t_i = conj(r_ir) r_ij).
             CAcc e;
             e.r0 = (r == 2 * q) ? 1.0 : 0.0;
             e.r1 = (r == 2 * q + 1) ? 1.0 : 0.0;
             e.i0 = 0.0;
             e.i1 = 0.0;
+            __syncwarp();                                   // every F1d read of the tile is done
 #pragma unroll
             for (int i = 0; i < 8; i++) {
-                const int sp = i * 4 + (i >> 1), sj = i * 4 + q, sr = i * 4 + (r >> 1);
-                const double t = shfl_d((i & 1) ? d.r1 : d.r0, sp);                 // Re a'_ii
-                const double ar0 = shfl_d(d.r0, sj), ai0 = shfl_d(d.i0, sj);        // a'_ij, my columns
-                const double ar1 = shfl_d(d.r1, sj), ai1 = shfl_d(d.i1, sj);
-                const double er0 = shfl_d(e.r0, sj), ei0 = shfl_d(e.i0, sj);        // E_ij, my columns
-                const double er1 = shfl_d(e.r1, sj), ei1 = shfl_d(e.i1, sj);
-                const double x0 = shfl_d(d.r0, sr), y0 = shfl_d(d.i0, sr);          // a'_i,r (my row)
-                const double x1 = shfl_d(d.r1, sr), y1 = shfl_d(d.i1, sr);
+                const int ie = (i + 4) & 7;
+                if (r == i) {
+                    tKK[oa0] = make_double2(d.r0, d.i0);
+                    tKK[oa1] = make_double2(d.r1, d.i1);
+                    tKK[sw(ie, 2 * q)] = make_double2(e.r0, e.i0);
+                    tKK[sw(ie, 2 * q + 1)] = make_double2(e.r1, e.i1);
+                }
+                __syncwarp();
+                const double t = tKK[sw(i, i)].x;                                    // Re a'_ii
+                const double2 a0 = tKK[sw(i, 2 * q)], a1 = tKK[sw(i, 2 * q + 1)];   // a'_ij, my columns
+                const double2 e0 = tKK[sw(ie, 2 * q)], e1 = tKK[sw(ie, 2 * q + 1)]; // E_ij, my columns
+                const double2 ar = tKK[sw(i, r)];                                    // a'_i,r (my row)
                 const bool bad = !(t > 0.0);
                 if (bad && inf == 0) inf = K * 8 + i + 1;
                 const double tt = bad ? 1.0 : t;
@@ -219,42 +366,29 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, int64_t batch, double2* X, int64
                 if (lane == 0) invs[K * 8 + i] = iv;
                 if (r == i) { acc_scale(d, iv); acc_scale(e, iv); }                  // row i of R, of E
                 if (r > i) {                                                          // rows below: -= conj(r_ir) r_i.
-                    const double2 w = make_double2(((r & 1) ? x1 : x0) * iv2, ((r & 1) ? y1 : y0) * iv2);
-                    acc_fms_conj(d, w, ar0, ai0, ar1, ai1);
-                    acc_fms_conj(e, w, er0, ei0, er1, ei1);
+                    const double2 w = make_double2(ar.x * iv2, ar.y * iv2);
+                    acc_fms_conj(d, w, a0.x, a0.y, a1.x, a1.y);
+                    acc_fms_conj(e, w, e0.x, e0.y, e1.x, e1.y);
                 }
             }
+            __syncwarp();
             // diagonal tile: R_KK in the strict upper half, E = R_KK^-H (lower, diagonal 1/r_kk)
             {
                 const bool up0 = r < 2 * q, up1 = r < 2 * q + 1;
                 tKK[oa0] = up0 ? make_double2(d.r0, d.i0) : make_double2(e.r0, e.i0);
                 tKK[oa1] = up1 ? make_double2(d.r1, d.i1) : make_double2(e.r1, e.i1);
             }
-            // ---- F1 + F2b per off-diagonal tile: R_KJ = E (A_KJ - sum_{P<K} R_PK^H R_PJ) (eq. 4)
-#pragma unroll 1
-            for (int J = K + 1; J < NTL; J++) {
-                double2* tKJ = TILE(K, J);
-                CAcc a;
-                acc_load(a, tKJ, oa0, oa1);
-#pragma unroll 1
-                for (int P = 0; P < K; P++) {
-                    const double2* tP = TILE(P, 0);
-#pragma unroll
-                    for (int s = 0; s < 2; s++) {
-                        const int ob = s ? ob1 : ob0;
-                        const double2 u = tP[64 * K + ob], v = tP[64 * J + ob];
-                        cmma(a, negd(u.x), u.y, negd(u.y), v.x, v.y);
-                    }
-                }
-                acc_store(a, tKJ, oa0, oa1);                                        // A'_KJ, read back as B
-                __syncwarp();
-                const double2 b0 = tKJ[ob0], b1 = tKJ[ob1];
-                __syncwarp();
-                CAcc x;
-                czero(x);
-                cmma(x, e.r0, e.i0, negd(e.i0), b0.x, b0.y);
-                cmma(x, e.r1, e.i1, negd(e.i1), b1.x, b1.y);
-                acc_store(x, tKJ, oa0, oa1);
+            DM_PHASE(3);
+            // ---- F1 + F2b of the off-diagonal tiles: R_KJ = E (A_KJ - sum_{P<K} R_PK^H R_PJ) (eq. 4)
+            switch (K) {
+                case 0: dm_factor_off<0>(Tw, L, e); break;
+                case 1: dm_factor_off<1>(Tw, L, e); break;
+                case 2: dm_factor_off<2>(Tw, L, e); break;
+                case 3: dm_factor_off<3>(Tw, L, e); break;
+                case 4: dm_factor_off<4>(Tw, L, e); break;
+                case 5: dm_factor_off<5>(Tw, L, e); break;
+                case 6: dm_factor_off<6>(Tw, L, e); break;
+                default: break;
             }
             __syncwarp();
         }
@@ -263,104 +397,70 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, int64_t batch, double2* X, int64
         // ========================================================== inversion, panels down
 #pragma unroll 1
         for (int K = NTL - 1; K >= 0; K--) {
-            const double2* rowK = TILE(K, 0);
-            const double2* tKK = rowK + 64 * K;
-            CAcc a[8];
-#pragma unroll
-            for (int J = 1; J < NTL; J++) czero(a[J]);
-            // ---- I1: C_KJ = sum_{M in T} R_KM X~_MJ (A = R_KM; B = X_MJ, or X_JM^H for M > J)
-#pragma unroll 1
-            for (int M = K + 1; M < NTL; M++) {
-                const double2* rowM = TILE(M, 0);
-#pragma unroll
-                for (int s = 0; s < 2; s++) {
-                    const double2 u = rowK[64 * M + (s ? oa1 : oa0)];
-                    const double nui = negd(u.y);
-#pragma unroll
-                    for (int J = 1; J < NTL; J++) {
-                        if (J > K) {
-                            double2 v;
-                            if (M <= J) v = rowM[64 * J + (s ? ob1 : ob0)];
-                            else { v = TILE(J, 0)[64 * M + (s ? oa1 : oa0)]; v.y = negd(v.y); }
-                            cmma(a[J], u.x, u.y, nui, v.x, v.y);
-                        }
-                    }
-                }
-            }
-            // ---- I2 + I3 per tile: X_KJ = -R_KK^-1 C_KJ (eqs. 22-24 for the rows of the panel,
-            //      R_KK^-1 = E^H from the diagonal tile's lower half), then V += R_KJ X_KJ^H and
-            //      X_KJ replaces R_KJ (every R_KT read of I1 is done)
-            double ra0, ia0, ra1, ia1;                                             // A = -R_KK^-1
-            {
-                const double2 w0 = tKK[ob0], w1 = tKK[ob1];                        // E(2q+s, r)
-                const bool v0 = 2 * q >= r, v1 = 2 * q + 1 >= r;
-                ra0 = v0 ? negd(w0.x) : 0.0; ia0 = v0 ? w0.y : 0.0;
-                ra1 = v1 ? negd(w1.x) : 0.0; ia1 = v1 ? w1.y : 0.0;
-            }
+            const double2* tKK = TILE(K, K);
             CAcc v;
             czero(v);
-#pragma unroll
-            for (int J = 1; J < NTL; J++) {
-                if (J > K) {
-                    acc_store(a[J], Ws, oa0, oa1);                                 // C_KJ, read back as B
-                    __syncwarp();
-                    const double2 c0 = Ws[ob0], c1 = Ws[ob1];
-                    __syncwarp();
-                    CAcc x;
-                    czero(x);
-                    cmma(x, ra0, ia0, negd(ia0), c0.x, c0.y);
-                    cmma(x, ra1, ia1, negd(ia1), c1.x, c1.y);
-                    double2* tKJ = TILE(K, J);
-                    const double2 u0 = tKJ[oa0], u1 = tKJ[oa1];                    // R_KJ
-                    cmma(v, u0.x, u0.y, negd(u0.y), x.r0, negd(x.i0));
-                    cmma(v, u1.x, u1.y, negd(u1.y), x.r1, negd(x.i1));
-                    acc_store(x, tKJ, oa0, oa1);
-                }
+            DM_PHASE(4);
+            // ---- I1 + I2 + I3 (v = V of the panel)
+            switch (K) {
+                case 0: dm_invert_off<0>(Tw, L, v); break;
+                case 1: dm_invert_off<1>(Tw, L, v); break;
+                case 2: dm_invert_off<2>(Tw, L, v); break;
+                case 3: dm_invert_off<3>(Tw, L, v); break;
+                case 4: dm_invert_off<4>(Tw, L, v); break;
+                case 5: dm_invert_off<5>(Tw, L, v); break;
+                case 6: dm_invert_off<6>(Tw, L, v); break;
+                default: break;
             }
-            // ---- I4: the diagonal tile; lane j (mod 8) owns column j of X_KK
+            DM_PHASE(5);
+            DM_PHASE(6);
+            // ---- I4: the diagonal tile by the recursion of eq. 23 with V added; lane j (mod 8) owns
+            //      column j.  The lower half of the tile (E, dead after I2) carries V transposed
+            //      (V_kj at slot (j, k)) and then, row by row, the mirror conj(x_kj) at slot (j, k),
+            //      which the diagonal lane k reads back as the lower part of its column.
             {
+                double2* D = TILE(K, K);
+                if (r <= 2 * q) D[sw(2 * q, r)] = make_double2(v.r0, v.i0);
+                if (r <= 2 * q + 1) D[sw(2 * q + 1, r)] = make_double2(v.r1, v.i1);
+                __syncwarp();
                 const int j = lane & 7;
-                double2 vc[8], xc[8];
+                double2 xc[8];
 #pragma unroll
-                for (int k = 0; k < 8; k++) {                                      // V_kj to lane j
-                    const int src = k * 4 + (j >> 1);
-                    const double v0 = shfl_d(v.r0, src), w0 = shfl_d(v.i0, src);
-                    const double v1 = shfl_d(v.r1, src), w1 = shfl_d(v.i1, src);
-                    vc[k] = (j & 1) ? make_double2(v1, w1) : make_double2(v0, w0);
-                    xc[k] = make_double2(0.0, 0.0);
-                }
+                for (int m = 0; m < 8; m++) xc[m] = make_double2(0.0, 0.0);
 #pragma unroll
                 for (int k = 7; k >= 0; k--) {
                     const double ik = invs[K * 8 + k];
                     // x_kj, j > k: -(1/r_kk)(V_kj + sum_{m>k} r_km x~_mj), two chains
-                    double2 s0 = vc[k], s1 = make_double2(0.0, 0.0);
+                    double2 s0 = D[sw(j, k)], s1 = make_double2(0.0, 0.0);
 #pragma unroll
                     for (int m = 7; m > k; m--) {
-                        const double2 rk = tKK[sw(k, m)];
-                        double2& s = ((7 - m) & 1) ? s1 : s0;
-                        s.x = fma(rk.x, xc[m].x, s.x); s.x = fma(-rk.y, xc[m].y, s.x);
-                        s.y = fma(rk.x, xc[m].y, s.y); s.y = fma(rk.y, xc[m].x, s.y);
+                        const double2 rk = D[sw(k, m)];
+                        double2& sa = ((7 - m) & 1) ? s1 : s0;
+                        sa.x = fma(rk.x, xc[m].x, sa.x); sa.x = fma(-rk.y, xc[m].y, sa.x);
+                        sa.y = fma(rk.x, xc[m].y, sa.y); sa.y = fma(rk.y, xc[m].x, sa.y);
                     }
-                    if (j > k) xc[k] = make_double2(-ik * (s0.x + s1.x), -ik * (s0.y + s1.y));
-                    // the row goes to the diagonal lane k as the lower part of its column (the
-                    // mirror), which forms x_kk = (1/r_kk)(1/r_kk - Re(V_kk + sum r_km conj(x_km)))
-                    double p = vc[k].x, p2 = 0.0;
+                    if (j > k) {
+                        xc[k] = make_double2(-ik * (s0.x + s1.x), -ik * (s0.y + s1.y));
+                        if (lane < 8) D[sw(j, k)] = make_double2(xc[k].x, negd(xc[k].y));   // the mirror
+                    }
+                    __syncwarp();
+                    if (j == k) {
+                        // x_kk = (1/r_kk)(1/r_kk - Re(V_kk + sum_{m>k} r_km conj(x_km)))
+                        double p = D[sw(k, k)].x, p2 = 0.0;
 #pragma unroll
-                    for (int m = 7; m > k; m--) {
-                        const double gx = shfl_d(xc[k].x, m), gy = shfl_d(xc[k].y, m);   // x_km
-                        if (j == k) {
-                            const double2 rk = tKK[sw(k, m)];
-                            xc[m] = make_double2(gx, negd(gy));
+                        for (int m = 7; m > k; m--) {
+                            const double2 g = D[sw(m, k)];                          // conj(x_km)
+                            const double2 rk = D[sw(k, m)];
+                            xc[m] = g;
                             double& pp = ((7 - m) & 1) ? p2 : p;
-                            pp = fma(rk.x, gx, pp);
-                            pp = fma(rk.y, gy, pp);
+                            pp = fma(rk.x, g.x, pp);
+                            pp = fma(-rk.y, g.y, pp);
                         }
+                        xc[k] = make_double2(ik * (ik - (p + p2)), 0.0);
                     }
-                    if (j == k) xc[k] = make_double2(ik * (ik - (p + p2)), 0.0);
                 }
                 __syncwarp();
                 if (lane < 8) {
-                    double2* D = TILE(K, K);
 #pragma unroll
                     for (int m = 0; m < 8; m++) D[sw(m, j)] = xc[m];
                 }
@@ -369,6 +469,7 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, int64_t batch, double2* X, int64
         }
         }
 
+        DM_PHASE(7);
         // ============================================ S5: store X, prefetch the next matrix
         const int64_t bn = b + stride;
         double2* Xb = X + b * sXm;
@@ -397,7 +498,13 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, int64_t batch, double2* X, int64
             }
         }
         if (lane == 0) info[b] = inf;
+        DM_PHASE(8);
     }
+#ifdef HPDINV_DMMA_PROF
+    DM_PHASE(8);
+    if (lane == 0)
+        for (int i = 0; i < 10; i++) atomicAdd(&dm::g_prof[i], (unsigned long long)prof_[i]);
+#endif
 #undef TILE
 }
 
