@@ -80,6 +80,17 @@ __device__ __forceinline__ void cmma(CAcc& c, double ar, double ai, double nai, 
     dmma(c.i0, c.i1, ai, br);
 }
 
+// the two halves of cmma: every first half of a k-step's tiles is issued before any second
+// half, so the dependent MMA pairs of one tile are a whole k-step apart
+__device__ __forceinline__ void cmma_h1(CAcc& c, double ar, double br, double bi) {
+    dmma(c.r0, c.r1, ar, br);
+    dmma(c.i0, c.i1, ar, bi);
+}
+__device__ __forceinline__ void cmma_h2(CAcc& c, double ai, double nai, double br, double bi) {
+    dmma(c.r0, c.r1, nai, bi);
+    dmma(c.i0, c.i1, ai, br);
+}
+
 __device__ __forceinline__ void acc_load(CAcc& c, const double2* tl, int o0, int o1) {
     const double2 a = tl[o0], b = tl[o1];
     c.r0 = a.x; c.i0 = a.y; c.r1 = b.x; c.i1 = b.y;
@@ -169,19 +180,30 @@ __device__ __forceinline__ void dm_factor_off(double2* __restrict__ Tw, const Dm
     CAcc a[NT_ > 0 ? NT_ : 1];
 #pragma unroll
     for (int u = 0; u < NT_; u++) acc_load(a[u], Tw + 64 * tidx(K, K + 1 + u), L.oa0, L.oa1);
+    // k-steps (P, s) software-pipelined: the next step's fragments are loaded before this step's MMAs
+    double2 w = Tw[64 * tidx(0, K) + L.ob0];
+    double2 v[NT_ > 0 ? NT_ : 1];
 #pragma unroll
-    for (int P = 0; P < K; P++) {
+    for (int u = 0; u < NT_; u++) v[u] = Tw[64 * tidx(0, K + 1 + u) + L.ob0];
 #pragma unroll
-        for (int s = 0; s < 2; s++) {
-            const int ob = s ? L.ob1 : L.ob0;
-            const double2 w = Tw[64 * tidx(P, K) + ob];                  // A = -conj(R_PK)^T
-            const double ar = negd(w.x), ai = w.y, nai = negd(w.y);
+    for (int st = 0; st < 2 * K; st++) {
+        const int P = st >> 1;
+        double2 wn = w, vn[NT_ > 0 ? NT_ : 1];
+        if (st + 1 < 2 * K) {
+            const int Pn = (st + 1) >> 1, obn = ((st + 1) & 1) ? L.ob1 : L.ob0;
+            wn = Tw[64 * tidx(Pn, K) + obn];                                 // A = -conj(R_PK)^T
 #pragma unroll
-            for (int u = 0; u < NT_; u++) {
-                const double2 v = Tw[64 * tidx(P, K + 1 + u) + ob];      // B = R_PJ
-                cmma(a[u], ar, ai, nai, v.x, v.y);
-            }
+            for (int u = 0; u < NT_; u++) vn[u] = Tw[64 * tidx(Pn, K + 1 + u) + obn];   // B = R_PJ
         }
+        const double ar = negd(w.x), ai = w.y, nai = negd(w.y);
+#pragma unroll
+        for (int u = 0; u < NT_; u++) cmma_h1(a[u], ar, v[u].x, v[u].y);
+#pragma unroll
+        for (int u = 0; u < NT_; u++) cmma_h2(a[u], ai, nai, v[u].x, v[u].y);
+        (void)P;
+        w = wn;
+#pragma unroll
+        for (int u = 0; u < NT_; u++) v[u] = vn[u];
     }
     // A' through its own tile, read back as the B operand of E A'
 #pragma unroll
@@ -216,20 +238,34 @@ __device__ __forceinline__ void dm_invert_off(double2* Tw, const DmLane& L, CAcc
     CAcc a[NT_];
 #pragma unroll
     for (int u = 0; u < NT_; u++) czero(a[u]);
+    // k-steps (m, s) software-pipelined: the next step's fragments are loaded before this step's MMAs
+    auto ldx = [&](int m, int s, int u) -> double2 {
+        double2 x;
+        if (m <= u) x = Tw[64 * tidx(M0 + m, M0 + u) + (s ? L.ob1 : L.ob0)];
+        else { x = Tw[64 * tidx(M0 + u, M0 + m) + (s ? L.oa1 : L.oa0)]; x.y = negd(x.y); }
+        return x;
+    };
+    double2 w = Tw[64 * tidx(K, M0) + L.oa0];
+    double2 x[NT_];
 #pragma unroll
-    for (int m = 0; m < NT_; m++) {
+    for (int u = 0; u < NT_; u++) x[u] = ldx(0, 0, u);
 #pragma unroll
-        for (int s = 0; s < 2; s++) {
-            const double2 w = Tw[64 * tidx(K, M0 + m) + (s ? L.oa1 : L.oa0)];   // A = R_KM
-            const double nwi = negd(w.y);
+    for (int st = 0; st < 2 * NT_; st++) {
+        double2 wn = w, xn[NT_];
+        if (st + 1 < 2 * NT_) {
+            const int mn = (st + 1) >> 1, sn = (st + 1) & 1;
+            wn = Tw[64 * tidx(K, M0 + mn) + (sn ? L.oa1 : L.oa0)];           // A = R_KM
 #pragma unroll
-            for (int u = 0; u < NT_; u++) {
-                double2 x;
-                if (m <= u) x = Tw[64 * tidx(M0 + m, M0 + u) + (s ? L.ob1 : L.ob0)];
-                else { x = Tw[64 * tidx(M0 + u, M0 + m) + (s ? L.oa1 : L.oa0)]; x.y = negd(x.y); }
-                cmma(a[u], w.x, w.y, nwi, x.x, x.y);
-            }
+            for (int u = 0; u < NT_; u++) xn[u] = ldx(mn, sn, u);
         }
+        const double nwi = negd(w.y);
+#pragma unroll
+        for (int u = 0; u < NT_; u++) cmma_h1(a[u], w.x, x[u].x, x[u].y);
+#pragma unroll
+        for (int u = 0; u < NT_; u++) cmma_h2(a[u], w.y, nwi, x[u].x, x[u].y);
+        w = wn;
+#pragma unroll
+        for (int u = 0; u < NT_; u++) x[u] = xn[u];
     }
     const double2* tKK = Tw + 64 * tidx(K, K);
     double ra0, ia0, ra1, ia1;                                          // A = -R_KK^-1
