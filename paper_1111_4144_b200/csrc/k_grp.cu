@@ -3,6 +3,10 @@
 #include "dispatch.h"
 #include "k_grp.cuh"
 
+#ifndef HPDINV_G16
+#define HPDINV_G16 4          // lanes per matrix at n = 16
+#endif
+
 namespace hpdinv {
 
 template <typename T, bool LDL>
@@ -21,7 +25,7 @@ static int launch_grp_t(const LaunchArgs& a) {
     if constexpr (sizeof(T) == 4) {
         switch (a.n) {
             HPDINV_GRP(9, 4) HPDINV_GRP(10, 4) HPDINV_GRP(11, 4) HPDINV_GRP(12, 4)
-            HPDINV_GRP(13, 4) HPDINV_GRP(14, 4) HPDINV_GRP(15, 4) HPDINV_GRP(16, 4)
+            HPDINV_GRP(13, 4) HPDINV_GRP(14, 4) HPDINV_GRP(15, 4) HPDINV_GRP(16, HPDINV_G16)
             HPDINV_GRP(32, 16)     // (32 lanes per matrix measured 10.3-13.1 ms at cfg5: SIMT imbalance)
             default: break;
         }

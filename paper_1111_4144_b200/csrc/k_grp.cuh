@@ -56,7 +56,11 @@ struct GrpShape {
     static constexpr int MPC = MPW * WARPS;           // matrices per CTA
     // n <= 16: 3 CTAs/SM caps ptxas at 170 registers (12 warps/SM); n = 32 (two 32-row columns
     // per lane) runs 8 warps/SM with up to 255 registers instead of spilling (measured faster)
-    static constexpr int MIN_BLOCKS = N <= 16 ? (12 / WARPS > 0 ? 12 / WARPS : 1) : (8 / WARPS > 0 ? 8 / WARPS : 1);
+#ifndef HPDINV_GRP_WSM16
+#define HPDINV_GRP_WSM16 12   // resident warps per SM at n <= 16 (register budget)
+#endif
+    static constexpr int MIN_BLOCKS = N <= 16 ? (HPDINV_GRP_WSM16 / WARPS > 0 ? HPDINV_GRP_WSM16 / WARPS : 1)
+                                              : (8 / WARPS > 0 ? 8 / WARPS : 1);
     static constexpr int P = sizeof(T) == 4 ? 2 : 1;  // complex elements per 16-byte load
     // packed row store: row i holds j = i..n-1 at offset roff(i) + (j - i), 16-byte aligned
     __host__ __device__ static constexpr int rlen(int i) { return ((N - i) + P - 1) / P * P; }
