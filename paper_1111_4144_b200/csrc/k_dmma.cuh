@@ -354,19 +354,36 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, int64_t batch, double2* X, int64
             DM_PHASE(1);
             double2* tKK = TILE(K, K);
             // ---- F1 on the diagonal tile: A_KK -= sum_{P<K} R_PK^H R_PK
-            CAcc d, d2;
+            // four accumulators (P even / odd x k-step s) and split MMA halves: the dependent MMA
+            // chain of the diagonal tile is a quarter as long
+            CAcc d, d1, d2, d3;
             acc_load(d, tKK, oa0, oa1);
+            czero(d1);
             czero(d2);
+            czero(d3);
+            {
+                int P = 0;
 #pragma unroll 1
-            for (int P = 0; P < K; P++) {
-                const double2* tPK = TILE(P, K);
-#pragma unroll
-                for (int s = 0; s < 2; s++) {
-                    const double2 u = tPK[s ? ob1 : ob0];                 // A = -conj(R_PK)^T, B = R_PK
-                    cmma((P & 1) ? d2 : d, negd(u.x), u.y, negd(u.y), u.x, u.y);
+                for (; P + 1 < K; P += 2) {
+                    const double2 u0 = TILE(P, K)[ob0], u1 = TILE(P, K)[ob1];       // A = -conj(R_PK)^T, B = R_PK
+                    const double2 w0 = TILE(P + 1, K)[ob0], w1 = TILE(P + 1, K)[ob1];
+                    cmma_h1(d, negd(u0.x), u0.x, u0.y);
+                    cmma_h1(d1, negd(u1.x), u1.x, u1.y);
+                    cmma_h1(d2, negd(w0.x), w0.x, w0.y);
+                    cmma_h1(d3, negd(w1.x), w1.x, w1.y);
+                    cmma_h2(d, u0.y, negd(u0.y), u0.x, u0.y);
+                    cmma_h2(d1, u1.y, negd(u1.y), u1.x, u1.y);
+                    cmma_h2(d2, w0.y, negd(w0.y), w0.x, w0.y);
+                    cmma_h2(d3, w1.y, negd(w1.y), w1.x, w1.y);
+                }
+                if (P < K) {
+                    const double2 u0 = TILE(P, K)[ob0], u1 = TILE(P, K)[ob1];
+                    cmma(d, negd(u0.x), u0.y, negd(u0.y), u0.x, u0.y);
+                    cmma(d1, negd(u1.x), u1.y, negd(u1.y), u1.x, u1.y);
                 }
             }
-            d.r0 += d2.r0; d.r1 += d2.r1; d.i0 += d2.i0; d.i1 += d2.i1;
+            d.r0 += (d1.r0 + d2.r0) + d3.r0; d.r1 += (d1.r1 + d2.r1) + d3.r1;
+            d.i0 += (d1.i0 + d2.i0) + d3.i0; d.i1 += (d1.i1 + d2.i1) + d3.i1;
             DM_PHASE(2);
             // ---- F2a: R_KK by the right-looking recursion of eqs. 3-4 on the accumulators, and
             //      E = R_KK^-H (the same row operations applied to I), for the panel solves.
@@ -511,26 +528,53 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, int64_t batch, double2* X, int64
         double2* Xb = X + b * sXm;
         const double nan = qnan<double>();
         const int rr = lane >> 3, cc = lane & 7;
-#pragma unroll 1
-        for (int I = 0; I < NTL; I++) {
-#pragma unroll 1
-            for (int J = I; J < NTL; J++) {
-                const double2* tl = TILE(I, J);
+        if (sXe == 1) {
+            // contiguous X: every address is the lane base plus a compile-time offset
+            double2* Xl = Xb + (rr * N + cc);
 #pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    const int ro = rr + 4 * h;
-                    double2 v = tl[sw(ro, cc)];
-                    double2 w = tl[sw(cc, ro)];                                     // (J, I) = conj^T
-                    w.y = negd(w.y);
-                    if (inf) { v = make_double2(nan, nan); w = v; }
-                    __stcs(Xb + int64_t((8 * I + ro) * N + 8 * J + cc) * sXe, v);
-                    if (I < J) __stcs(Xb + int64_t((8 * J + ro) * N + 8 * I + cc) * sXe, w);
+            for (int I = 0; I < NTL; I++) {
+#pragma unroll
+                for (int J = I; J < NTL; J++) {
+                    const double2* tl = Tw + 64 * tidx(I, J);
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const int ro = rr + 4 * h;
+                        double2 v = tl[sw(ro, cc)];
+                        double2 w = tl[sw(cc, ro)];                                 // (J, I) = conj^T
+                        w.y = negd(w.y);
+                        if (inf) { v = make_double2(nan, nan); w = v; }
+                        __stcs(Xl + ((8 * I + 4 * h) * N + 8 * J), v);
+                        if (I < J) __stcs(Xl + ((8 * J + 4 * h) * N + 8 * I), w);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0 && bn < batch) {             // row I is free: load it for the next matrix
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    load_row(Tw, &tmA, I, bn, &bar[I]);
                 }
             }
-            __syncwarp();
-            if (lane == 0 && bn < batch) {                 // row I is free: load it for the next matrix
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                load_row(Tw, &tmA, I, bn, &bar[I]);
+        } else {
+#pragma unroll 1
+            for (int I = 0; I < NTL; I++) {
+#pragma unroll 1
+                for (int J = I; J < NTL; J++) {
+                    const double2* tl = TILE(I, J);
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const int ro = rr + 4 * h;
+                        double2 v = tl[sw(ro, cc)];
+                        double2 w = tl[sw(cc, ro)];                                 // (J, I) = conj^T
+                        w.y = negd(w.y);
+                        if (inf) { v = make_double2(nan, nan); w = v; }
+                        __stcs(Xb + int64_t((8 * I + ro) * N + 8 * J + cc) * sXe, v);
+                        if (I < J) __stcs(Xb + int64_t((8 * J + ro) * N + 8 * I + cc) * sXe, w);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0 && bn < batch) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    load_row(Tw, &tmA, I, bn, &bar[I]);
+                }
             }
         }
         if (lane == 0) info[b] = inf;
