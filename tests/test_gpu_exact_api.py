@@ -164,6 +164,36 @@ def test_determinism_and_slicing_invariance():
             assert np.array_equal(np.concatenate(parts), X1)
 
 
+def test_dmma_schedule_invariance():
+    """k_dmma (persistent, one matrix per warp, TMA prefetch of the next matrix during the store
+    phase): the output bits do not depend on which warp inverts which matrix or on how many
+    matrices a warp chains -- repeated runs, shards of the batch (different grids), in-place
+    and padded-stride runs are bitwise equal.  compute-sanitizer is closed on this pool
+    (profiles/r02_sanitizer_closed.txt); a race on the shared tiles or the mbarriers would show
+    up here as a schedule-dependent result."""
+    cfg = wl.CONFIGS[4]
+    batch = 3001                                       # > 148 x 6 warps: every warp chains matrices
+    A = wl.generate(cfg, 0, batch, device="cuda")
+    assert hp.kernel_name("chol", cfg.dtype, batch, cfg.n, (A.stride(0), A.stride(2))) == "k_dmma<c128,chol>"
+    X1, i1 = hp.invert(A, "chol")
+    X2, i2 = hp.invert(A, "chol")
+    torch.cuda.synchronize()
+    assert torch.equal(X1, X2) and torch.equal(i1, i2) and int(i1.abs().sum()) == 0
+    for world in (2, 7, 40):                           # 40 shards: grids of 13 CTAs, one matrix per warp
+        for r in range(world):
+            s, c = wl.shard(r, world, batch)
+            Xs, _ = hp.invert(A[s:s + c].clone(), "chol")
+            assert torch.equal(Xs, X1[s:s + c])
+    Ain = A.clone()
+    hp.invert(Ain, "chol", X=Ain)                      # in place
+    pad = torch.zeros(batch, 64 * 64 + 8, dtype=A.dtype, device="cuda")   # padded matrix stride
+    pad[:, :4096] = A.reshape(batch, 4096)
+    Ap = torch.as_strided(pad, (batch, 64, 64), (64 * 64 + 8, 64, 1))
+    Xp, _ = hp.invert(Ap, "chol")
+    torch.cuda.synchronize()
+    assert torch.equal(Ain, X1) and torch.equal(Xp.contiguous(), X1)
+
+
 def test_kernel_names():
     assert hp.kernel_name("chol", torch.complex64, 1 << 20, 8, (1, 1 << 20)) is not None
     assert hp.kernel_name("chol", torch.complex64, 8, 65) is None
