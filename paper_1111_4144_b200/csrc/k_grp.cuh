@@ -69,7 +69,8 @@ struct GrpShape {
     static constexpr int ESZ = int(sizeof(cplx<T>));
     // per matrix: row store + X row buffer (n, padded) + reciprocals (n reals); the stride in
     // bytes is 16 mod 128 so the MPW groups of a warp hit distinct 16-byte bank quads
-    static constexpr int raw_bytes = (RSZ + (N + P - 1) / P * P) * ESZ + ((N * int(sizeof(T)) + 15) / 16) * 16;
+    static constexpr int RB = (N + P - 1) / P * P;     // one X row buffer (two, alternating)
+    static constexpr int raw_bytes = (RSZ + 2 * RB) * ESZ + ((N * int(sizeof(T)) + 15) / 16) * 16;
     static constexpr int MSTR_B = ((raw_bytes + 127) / 128) * 128 + 16;
     static constexpr size_t smem_bytes = size_t(MPC) * MSTR_B;
 };
@@ -113,8 +114,8 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
     b = valid ? b : batch - 1;                        // the tail recomputes (never stores) the last matrix
     unsigned char* mbase = smem_raw + size_t(mloc) * Sh::MSTR_B;
     V* Rs = reinterpret_cast<V*>(mbase);                              // packed R rows
-    V* rowbuf = Rs + Sh::RSZ;                                         // X row k
-    T* invs = reinterpret_cast<T*>(rowbuf + (N + P - 1) / P * P);     // 1/r_kk or 1/d_k
+    V* rowbuf0 = Rs + Sh::RSZ;                                        // X row k (k odd: + RB)
+    T* invs = reinterpret_cast<T*>(rowbuf0 + 2 * Sh::RB);             // 1/r_kk or 1/d_k
 
     // ---------------------------------------------------------------- S1: load columns
     // (entries below the diagonal of a column are dead storage; Im a_jj is never read)
@@ -190,13 +191,15 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
                 }
             }
         }
-        __syncwarp();
+        // (no trailing __syncwarp: row i+1 of the row store is a different region, so the next
+        //  step's pivot chain may overlap this step's update)
     }
 
     // ------------------------------------------------ S3/S4: proposed inversion, rows k = n..1
 #pragma unroll
     for (int k = N - 1; k >= 0; k--) {
         const int qk = k % G, sk = k / G;
+        V* rowbuf = rowbuf0 + (k & 1) * Sh::RB;          // alternating: no reuse hazard between rows
         const V* Rk = Rs + Sh::roff(k);
         const T ik = invs[k];
         V rk[N];                                        // r_km, m > k
@@ -254,7 +257,6 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
             }
             col[sk][k] = mk<T>(LDL ? ik - pl : ik * (ik - pl), T(0));
         }
-        __syncwarp();
     }
 
     // ------------------------------------------------------------------ S5: mirror + store
