@@ -302,19 +302,28 @@ class CudaBackend:
         return st
 
     def maybe_graph(self, st, per_step_s: float, mode: str):
-        """Launch-bound per-rank batches (cfg1, or any slice whose kernel is a few tens of µs)
-        replay the step from a CUDA graph so the host-side Python/ctypes overhead does not pose
-        as kernel time."""
+        """Launch-bound per-rank batches (cfg1, or a strong-scaled slice whose kernel is a few
+        tens of µs) replay the step from CUDA graphs so the host-side Python/ctypes overhead does
+        not pose as kernel time: one graph holds G consecutive steps (G kernel nodes, G * the
+        kernel time >= ~100 µs) and one graph a single step, so exactly `steps` launches are
+        timed.  Returns (multi_fn, G, single_fn) or a plain per-step callable."""
         use = mode == "on" or (mode == "auto" and per_step_s < 60e-6)
         if not use:
             return st["step"], "direct C-ABI call per step"
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
+        G = max(1, min(64, int(100e-6 / max(per_step_s, 1e-6))))
+        g1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1):
             st["step"]()
-        graph.replay()
+        gG = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gG):
+            for _ in range(G):
+                st["step"]()
+        g1.replay()
+        gG.replay()
         self.sync()
-        st["graph"] = graph
-        return graph.replay, "CUDA graph of the C-ABI call (one kernel node), replayed per step"
+        st["graphs"] = (g1, gG)
+        return (gG.replay, G, g1.replay), ("CUDA graphs of the C-ABI call (%d steps = %d kernel nodes per "
+                                           "replay, and a one-step graph for the remainder)" % (G, G))
 
     def nonzero_info(self, st):
         return int((st["info"] != 0).sum().item())
@@ -325,20 +334,30 @@ class CudaBackend:
 
 def timed_loop(step, steps: int, warmup: int, backend, dist: Dist):
     """W untimed warm-up steps, then exactly `steps` timed steps between a barrier +
-    synchronize on both sides.  Returns (ms_per_step, kernel_ms, wall_span_ms) reduced over
-    the ranks: the max of the per-rank device times; the wall span is the host-clock interval
-    from the earliest rank's start to the latest rank's end (ranks share one host clock)."""
-    for _ in range(warmup):
-        step()
+    synchronize on both sides.  `step` is a per-step callable or (multi_fn, G, single_fn): a
+    replay of G steps and of one step (launch-bound batches, see CudaBackend.maybe_graph).
+    Returns (ms_per_step, kernel_ms, wall_span_ms) reduced over the ranks: the max of the
+    per-rank device times (kernel_ms = event time around the launches / steps); the wall span
+    is the host-clock interval from the earliest rank's start to the latest rank's end (ranks
+    share one host clock)."""
+    if isinstance(step, tuple):
+        multi, G, single = step
+        plan = [(multi, G)] * (steps // G) + [(single, 1)] * (steps % G)
+        warm = [(multi, G)] * (warmup // G) + [(single, 1)] * (warmup % G)
+    else:
+        plan = [(step, 1)] * steps
+        warm = [(step, 1)] * warmup
+    for fn, _ in warm:
+        fn()
     backend.sync()
     dist.barrier()
     backend.sync()
     t_host0 = time.time()
     t0 = backend.event()
     evs = []
-    for _ in range(steps):
+    for fn, _ in plan:
         a = backend.event()
-        step()
+        fn()
         evs.append((a, backend.event()))
     t1 = backend.event()
     backend.sync()
