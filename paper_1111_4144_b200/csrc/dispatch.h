@@ -43,6 +43,8 @@ int launch_blk(int dtype, bool ldl, const LaunchArgs& a);       // k_blk.cu (n =
 int launch_dmma(const LaunchArgs& a);                            // k_dmma.cu (c128, n = 64, Cholesky, AoS A)
 bool dmma_accepts(int dtype, bool ldl, int n, int64_t sAm, int64_t sAe);
 int launch_solve(int dtype, bool ldl, const SolveArgs& a);      // k_solve.cu (any n <= 64)
+int launch_grp_solve(int dtype, bool ldl, const SolveArgs& a);  // k_grp.cu (c64 n = 9..16, 32)
+bool grp_solve_accepts(int dtype, int n, int64_t sAe);
 const char* solve_kernel_name(int dtype, bool ldl, int n);
 int launch_base(int method, int dtype, const LaunchArgs& a);    // k_base.cu (methods 2, 3)
 const char* base_kernel_name(int method, int dtype, int n);

@@ -43,6 +43,49 @@ static int launch_grp_t(const LaunchArgs& a) {
     return int(cudaGetLastError());
 }
 
+template <typename T, bool LDL>
+static int launch_grp_solve_t(const SolveArgs& a) {
+    using V = cplx<T>;
+    using fn_t = void (*)(int64_t, const V*, int64_t, int64_t, const V*, int64_t, int64_t, V*, int64_t, int64_t, int32_t*);
+    fn_t fn = nullptr;
+    size_t smem = 0;
+    int mpc = 1, threads = 0;
+#define HPDINV_GRPS(NN, GG)                         \
+    case NN:                                        \
+        fn = k_grp_solve<T, NN, GG, LDL>;           \
+        smem = GrpShape<T, NN, GG>::smem_bytes;     \
+        mpc = GrpShape<T, NN, GG>::MPC;             \
+        threads = GrpShape<T, NN, GG>::THREADS;     \
+        break;
+    if constexpr (sizeof(T) == 4) {
+        switch (a.n) {
+            HPDINV_GRPS(9, 4) HPDINV_GRPS(10, 4) HPDINV_GRPS(11, 4) HPDINV_GRPS(12, 4)
+            HPDINV_GRPS(13, 4) HPDINV_GRPS(14, 4) HPDINV_GRPS(15, 4) HPDINV_GRPS(16, 4)
+            HPDINV_GRPS(32, 16)
+            default: break;
+        }
+    }
+#undef HPDINV_GRPS
+    if (!grp_strides_ok(a.sAe, 0, sizeof(V))) fn = nullptr;
+    if (!fn) return kNoKernel;
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
+    if (e != cudaSuccess) return int(e);
+    const int64_t blocks = (a.batch + mpc - 1) / mpc;
+    fn<<<unsigned(blocks), threads, smem, a.stream>>>(a.batch, static_cast<const V*>(a.A), a.sAm, a.sAe,
+                                                     static_cast<const V*>(a.Y), a.sYm, a.sYe,
+                                                     static_cast<V*>(a.X), a.sXm, a.sXe, a.info);
+    return int(cudaGetLastError());
+}
+
+bool grp_solve_accepts(int dtype, int n, int64_t sAe) {
+    return dtype == 0 && ((n >= 9 && n <= 16) || n == 32) && grp_strides_ok(sAe, 0, 8);
+}
+
+int launch_grp_solve(int dtype, bool ldl, const SolveArgs& a) {
+    if (dtype != 0) return kNoKernel;
+    return ldl ? launch_grp_solve_t<float, true>(a) : launch_grp_solve_t<float, false>(a);
+}
+
 int launch_grp(int dtype, bool ldl, const LaunchArgs& a) {
     if (dtype == 0) return ldl ? launch_grp_t<float, true>(a) : launch_grp_t<float, false>(a);
     return kNoKernel;

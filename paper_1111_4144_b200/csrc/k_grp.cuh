@@ -95,35 +95,22 @@ __device__ __forceinline__ void lds_pair(const cplx<T>* p, int o, cplx<T>& e0, c
 }
 }  // namespace grp
 
+// S1 + S2 of a lane group (shared by the inversion k_grp and the solve k_grp_solve): lane q
+// loads the upper part of its columns j = q + G*s and runs the right-looking factorisation with
+// the packed row store Rs; returns info.  See k_grp for the design notes.
 template <typename T, int N, int GG, bool LDL>
-__global__ void __launch_bounds__(GrpShape<T, N, GG>::THREADS, GrpShape<T, N, GG>::MIN_BLOCKS)
-k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
-      cplx<T>* X, int64_t sXm, int64_t sXe, int32_t* __restrict__ info)
-{
+__device__ __forceinline__ int grp_factor(cplx<T> (&col)[GrpShape<T, N, GG>::C][N], const cplx<T>* __restrict__ Am,
+                                          int64_t sAe, int q, cplx<T>* Rs, T* invs) {
     using Sh = GrpShape<T, N, GG>;
     using V = cplx<T>;
     constexpr int G = Sh::G, C = Sh::C, P = Sh::P;
     constexpr unsigned FULL = 0xffffffffu;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int q = lane & (G - 1), g = lane / G;
-    const int mloc = warp * Sh::MPW + g;
-    int64_t b = int64_t(blockIdx.x) * Sh::MPC + mloc;
-    const bool valid = b < batch;
-    b = valid ? b : batch - 1;                        // the tail recomputes (never stores) the last matrix
-    unsigned char* mbase = smem_raw + size_t(mloc) * Sh::MSTR_B;
-    V* Rs = reinterpret_cast<V*>(mbase);                              // packed R rows
-    V* rowbuf0 = Rs + Sh::RSZ;                                        // X row k (k odd: + RB)
-    T* invs = reinterpret_cast<T*>(rowbuf0 + 2 * Sh::RB);             // 1/r_kk or 1/d_k
-
     // ---------------------------------------------------------------- S1: load columns
     // (entries below the diagonal of a column are dead storage; Im a_jj is never read)
-    V col[C][N];
     {
         // element (l, j = q + G*s): lane base + (l*n + G*s) * plane stride; the plane stride in
         // bytes is < 2^32 (checked by the launcher), so each address is one IMAD.WIDE
-        const char* Ab = reinterpret_cast<const char*>(A + b * sAm + q * sAe);
+        const char* Ab = reinterpret_cast<const char*>(Am + q * sAe);
         const uint32_t seA = uint32_t(sAe * int64_t(sizeof(V)));
 #pragma unroll
         for (int s = 0; s < C; s++) {
@@ -194,6 +181,34 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
         // (no trailing __syncwarp: row i+1 of the row store is a different region, so the next
         //  step's pivot chain may overlap this step's update)
     }
+
+    return inf;
+}
+
+template <typename T, int N, int GG, bool LDL>
+__global__ void __launch_bounds__(GrpShape<T, N, GG>::THREADS, GrpShape<T, N, GG>::MIN_BLOCKS)
+k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
+      cplx<T>* X, int64_t sXm, int64_t sXe, int32_t* __restrict__ info)
+{
+    using Sh = GrpShape<T, N, GG>;
+    using V = cplx<T>;
+    constexpr int G = Sh::G, C = Sh::C, P = Sh::P;
+    constexpr unsigned FULL = 0xffffffffu;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q = lane & (G - 1), g = lane / G;
+    const int mloc = warp * Sh::MPW + g;
+    int64_t b = int64_t(blockIdx.x) * Sh::MPC + mloc;
+    const bool valid = b < batch;
+    b = valid ? b : batch - 1;                        // the tail recomputes (never stores) the last matrix
+    unsigned char* mbase = smem_raw + size_t(mloc) * Sh::MSTR_B;
+    V* Rs = reinterpret_cast<V*>(mbase);                              // packed R rows
+    V* rowbuf0 = Rs + Sh::RSZ;                                        // X row k (k odd: + RB)
+    T* invs = reinterpret_cast<T*>(rowbuf0 + 2 * Sh::RB);             // 1/r_kk or 1/d_k
+
+    V col[C][N];
+    int inf = grp_factor<T, N, GG, LDL>(col, A + b * sAm, sAe, q, Rs, invs);
 
     // ------------------------------------------------ S3/S4: proposed inversion, rows k = n..1
 #pragma unroll
@@ -276,6 +291,105 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
                     grp::st(reinterpret_cast<V*>(Xrow + uint64_t(uint32_t(m * N + G * s)) * seX),
                             inf ? mk<T>(nan, nan) : col[s][m]);
             }
+        }
+        if (q == 0) info[b] = inf;
+    }
+}
+
+// k_grp_solve -- SURVEY §8(f) f1 with the lane-group mapping (c64, n = 9..16 with 4 lanes per
+// system, n = 32 with 16): the factorisation of k_grp (grp_factor), then the two O(n^2) sweeps
+// on the lane-distributed columns -- lane q holds y_j, then b_j / w_j, then x_j for its columns
+// j = q + G*s:
+//   forward  R* b = y (eq. 6; LDL R* z = y, w = D^-1 z, eq. 13): step k, the owner of column k
+//            finalises b_k and broadcasts it by shuffle; each lane updates its y_j, j > k, with
+//            conj(r_kj) b_k -- r_kj is row k of its own register column;
+//   backward R x = b (eq. 7; LDL R x = w, eq. 14): step k (descending), each lane forms its share
+//            sum_{own j > k} r_kj x_j from its register column, the G lanes combine it by
+//            shuffles, and the owner of column k finalises x_k.
+template <typename T, int N, int GG, bool LDL>
+__global__ void __launch_bounds__(GrpShape<T, N, GG>::THREADS, GrpShape<T, N, GG>::MIN_BLOCKS)
+k_grp_solve(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
+            const cplx<T>* __restrict__ Y, int64_t sYm, int64_t sYe, cplx<T>* Xv, int64_t sXm, int64_t sXe,
+            int32_t* __restrict__ info)
+{
+    using Sh = GrpShape<T, N, GG>;
+    using V = cplx<T>;
+    constexpr int G = Sh::G, C = Sh::C;
+    constexpr unsigned FULL = 0xffffffffu;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q = lane & (G - 1), g = lane / G;
+    const int mloc = warp * Sh::MPW + g;
+    int64_t b = int64_t(blockIdx.x) * Sh::MPC + mloc;
+    const bool valid = b < batch;
+    b = valid ? b : batch - 1;                        // the tail recomputes (never stores) the last system
+    unsigned char* mbase = smem_raw + size_t(mloc) * Sh::MSTR_B;
+    V* Rs = reinterpret_cast<V*>(mbase);
+    T* invs = reinterpret_cast<T*>(Rs + Sh::RSZ + 2 * Sh::RB);
+
+    V yv[C];
+#pragma unroll
+    for (int s = 0; s < C; s++) {
+        const int j = q + G * s;
+        yv[s] = (j < N) ? Y[b * sYm + int64_t(j) * sYe] : czero<T>();
+    }
+    V col[C][N];
+    const int inf = grp_factor<T, N, GG, LDL>(col, A + b * sAm, sAe, q, Rs, invs);
+    __syncwarp();
+
+    // ---- forward: R* b = y (Cholesky b_k = y'_k / r_kk; LDL z_k = y'_k, w_k = z_k / d_k)
+#pragma unroll
+    for (int k = 0; k < N; k++) {
+        const int qk = k % G, sk = k / G;
+        const T ik = invs[k];
+        V bk = yv[sk];                                   // owner's finished y'_k
+        if (!LDL) bk = cscale(bk, ik);
+        bk = mk<T>(__shfl_sync(FULL, bk.x, qk, G), __shfl_sync(FULL, bk.y, qk, G));
+        if (q == qk) yv[sk] = LDL ? cscale(bk, ik) : bk;   // b_k (LDL: w_k)
+#pragma unroll
+        for (int s = 0; s < C; s++) {
+            const int j = q + G * s;
+            if (G * s + G - 1 > k && j > k) {            // y'_j -= conj(r_kj) b_k
+                const V r = col[s][k];
+                V y = yv[s];
+                y.x = fmaf(-r.x, bk.x, y.x); y.x = fmaf(-r.y, bk.y, y.x);
+                y.y = fmaf(-r.x, bk.y, y.y); y.y = fmaf(r.y, bk.x, y.y);
+                yv[s] = y;
+            }
+        }
+    }
+    // ---- backward: R x = b (Cholesky x_k = (b_k - sum) / r_kk; LDL x_k = w_k - sum)
+#pragma unroll
+    for (int k = N - 1; k >= 0; k--) {
+        const int qk = k % G, sk = k / G;
+        V p = czero<T>();
+#pragma unroll
+        for (int s = 0; s < C; s++) {
+            const int j = q + G * s;
+            if (G * s + G - 1 > k && j > k) {            // r_kj x_j over this lane's columns
+                const V r = col[s][k], x = yv[s];
+                p.x = fmaf(r.x, x.x, p.x); p.x = fmaf(-r.y, x.y, p.x);
+                p.y = fmaf(r.x, x.y, p.y); p.y = fmaf(r.y, x.x, p.y);
+            }
+        }
+#pragma unroll
+        for (int off = 1; off < G; off <<= 1) {
+            p.x += __shfl_xor_sync(FULL, p.x, off, G);
+            p.y += __shfl_xor_sync(FULL, p.y, off, G);
+        }
+        if (q == qk) {
+            const V w = yv[sk];
+            const V d = mk<T>(w.x - p.x, w.y - p.y);
+            yv[sk] = LDL ? d : cscale(d, invs[k]);
+        }
+    }
+    if (valid) {
+        const T nan = qnan<T>();
+#pragma unroll
+        for (int s = 0; s < C; s++) {
+            const int j = q + G * s;
+            if (j < N) Xv[b * sXm + int64_t(j) * sXe] = inf ? mk<T>(nan, nan) : yv[s];
         }
         if (q == 0) info[b] = inf;
     }

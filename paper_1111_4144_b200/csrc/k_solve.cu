@@ -29,6 +29,11 @@ static int launch_solve_t(const SolveArgs& a) {
                                                             X, a.sXm, a.sXe, a.info);
         return int(cudaGetLastError());
     }
+    // c64 n = 9..16 and 32: the lane-group solve (k_grp_solve); otherwise the CTA fallback
+    if (sizeof(T) == 4) {
+        const int rc = launch_grp_solve(0, LDL, a);
+        if (rc != kNoKernel) return rc;
+    }
     auto gfn = k_solve_gen<T, LDL>;
     const size_t smem = solve_gen_smem_bytes<T>(a.n);
     cudaError_t e = ensure_smem(reinterpret_cast<const void*>(gfn), smem);
@@ -50,6 +55,8 @@ const char* solve_kernel_name(int dtype, bool ldl, int n) {
         {{"k_solve_gen<c64,chol>", "k_solve_gen<c64,ldl>"}, {"k_solve_gen<c128,chol>", "k_solve_gen<c128,ldl>"}},
     };
     const bool reg = n <= reg_max_n(dtype);
+    if (!reg && dtype == 0 && ((n >= 9 && n <= 16) || n == 32))
+        return ldl ? "k_grp_solve<c64,ldl>" : "k_grp_solve<c64,chol>";
     return names[reg ? 0 : 1][dtype][ldl ? 1 : 0];
 }
 

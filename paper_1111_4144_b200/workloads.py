@@ -62,6 +62,11 @@ CONFIGS = {
     6: Config(6, 8, torch.complex64, 1 << 20, "chol", "soa", "bbh", 8.0, 0.1,
               "2^20 c64 HPD 8x8 systems A x = y (cfg2 matrices, y ~ CN(0,I)), Cholesky solve eqs. 5-7, "
               "interleaved", task="solve"),
+    # SURVEY §8(f) f1 at the lane-group sizes: the cfg3 matrices (n = 16) with one right-hand
+    # side each, solved by eqs. 5-7 (k_grp_solve)
+    9: Config(9, 16, torch.complex64, 1 << 22, "chol", "soa", "bbh", 16.0, 0.01,
+              "2^22 c64 HPD 16x16 systems A x = y (cfg3 matrices, y ~ CN(0,I)), Cholesky solve eqs. 5-7, "
+              "interleaved", task="solve"),
     # SURVEY §8(f) f2 (next row): non-Hermitian D = I + B / (2 sqrt(n)), B i.i.d. CN(0,1) (a
     # channel-like matrix near the identity; the paper gives no workload), D^-1 = D* (DD*)^-1
     7: Config(7, 8, torch.complex64, 1 << 20, "chol", "soa", "nonherm", 2.0 * 8 ** 0.5, 1.0,
