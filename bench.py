@@ -455,7 +455,7 @@ def e2e_measure(args, cfg: wl.Config, st, world: int, dist: Dist, dev, steps: in
     store = st["store"]
     stream = torch.cuda.current_stream(dev)
     e2e_steps = max(3, min(steps, 10))
-    chunk = max(4096, B // 8)
+    chunk = max(4096, B // 8)          # 8 chunks: measured best of 4 / 8 / 16 / 32 at cfg2
     if cfg.task == "solve":
         A_host = store.cpu().pin_memory()
         Y_host = st["ystore"].cpu().pin_memory()
