@@ -54,13 +54,23 @@ int launch_dmma(const LaunchArgs& a) {
                                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return b0 == 0 ? kNoKernel : int(cudaErrorInvalidValue);
+        // X by TMA bulk stores when it is contiguous row-major per matrix (else per-lane stores)
+        CUtensorMap tmx;
+        int xtma = 0;
+        if (a.sXe == 1 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) {
+            const cuuint64_t xstr[2] = {cuuint64_t(dm::N) * 16, cuuint64_t(a.sXm) * 16};
+            xtma = enc(&tmx, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, X, dims, xstr, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        }
+        if (!xtma) tmx = tm;
         // persistent: one CTA of WPB warps per SM (WPB matrices in flight per SM)
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t need = (nb + dm::WPB - 1) / dm::WPB;
         const unsigned grid = unsigned(need < sms ? need : sms);
-        k_dmma<<<grid, dm::NT, dm::SMEM, a.stream>>>(tm, nb, X, a.sXm, a.sXe, a.info + b0);
+        k_dmma<<<grid, dm::NT, dm::SMEM, a.stream>>>(tm, tmx, xtma, nb, X, a.sXm, a.sXe, a.info + b0);
         if ((e = cudaGetLastError()) != cudaSuccess) return int(e);
     }
     return 0;

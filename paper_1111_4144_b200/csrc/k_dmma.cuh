@@ -10,9 +10,10 @@
 // Why one matrix per warp: no block-level barrier anywhere -- the serial phases of one warp
 // (pivots, the in-tile substitutions, the diagonal-tile inversion) overlap the DMMA phases of
 // the other warps of the SM -- and 255 registers per thread (6 warps per SM, 216 KB of tiles).
-// Persistent: warp w of CTA c inverts matrices c*6 + w, + 6*gridDim, ...; while it stores
-// matrix b it already loads matrix b + 6*gridDim into the tiles it has stored (TMA, one
-// mbarrier per tile row, so panel K of the next matrix waits only for tile row K).
+// Persistent: CTA c inverts matrices c*6 + w + 6*gridDim*k (its warps take them from a shared
+// counter, the first six statically); while a warp stores matrix b it already loads its next
+// matrix into the tiles it has stored (TMA, one mbarrier per tile row, so panel K of the next
+// matrix waits only for tile row K).
 //
 // Storage (per warp, 36 KB): only the 36 UPPER 8 x 8 tiles (I <= J) of the working matrix,
 // complex interleaved, 1 KB per tile; element (r, c) of a tile at 16-byte slot r*8 + (c ^ r)
@@ -51,7 +52,7 @@ constexpr int WPB = 6;                               // warps (matrices) per CTA
 constexpr int NT = 32 * WPB;
 constexpr int TILES_B = NTILE * 1024;                // 36 tiles per warp
 constexpr int AUX_B = 64 * 8 + 8 * 8;                // per warp: 1/r_kk (64 doubles), 8 mbarriers
-constexpr int SMEM = WPB * (TILES_B + AUX_B) + 1024; // + alignment slack (TMA 128B swizzle)
+constexpr int SMEM = WPB * (TILES_B + AUX_B) + 16 + 1024; // + the CTA's matrix counter + alignment slack (TMA 128B swizzle)
 
 __host__ __device__ constexpr int tidx(int I, int J) { return I * NTL - I * (I - 1) / 2 + (J - I); }
 // first slot of tile row I (tile (I, J) = rowbase(I) + 64 J, double2 units; J >= I only)
@@ -141,6 +142,19 @@ __device__ __forceinline__ void tma_load_tile(void* dst, const CUtensorMap* tm, 
         ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
 }
+// tile (I, J) of matrix b from shared memory to X (the map's 128-byte swizzle undoes the slots)
+__device__ __forceinline__ void tma_store_tile(const CUtensorMap* tm, const void* src, int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];"
+        ::"l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int PENDING>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(PENDING) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // tile row I of matrix b: arm its barrier and load tiles (I, I..7)
 __device__ __forceinline__ void load_row(double2* Tw, const CUtensorMap* tm, int I, int64_t b, uint64_t* bar) {
     mbar_expect_tx(bar, unsigned(NTL - I) * 1024u);
@@ -308,8 +322,8 @@ __device__ __forceinline__ void dm_invert_off(double2* Tw, const DmLane& L, CAcc
 // {16, 8, 1} (one 8 x 8 complex tile), 128-byte swizzle.  X: any layout (element (i, j) of
 // matrix b at X[b*sXm + (i*n + j)*sXe]); info[b] as for every kernel.
 __global__ void __launch_bounds__(dm::NT, 1)
-k_dmma(const __grid_constant__ CUtensorMap tmA, int64_t batch, double2* X, int64_t sXm, int64_t sXe,
-       int32_t* __restrict__ info)
+k_dmma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX, int xtma,
+       int64_t batch, double2* X, int64_t sXm, int64_t sXe, int32_t* __restrict__ info)
 {
     using namespace dm;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -327,7 +341,13 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, int64_t batch, double2* X, int64
     const int ob0 = sw(2 * q, r), ob1 = sw(2 * q + 1, r);
     const DmLane L{oa0, oa1, ob0, ob1, r, q};
 
+    // The CTA's j-th matrix is m(j) = (j / WPB) * stride + blockIdx.x * WPB + j % WPB; its warps take
+    // j from a shared-memory counter (the first WPB statically), so the warps that have an SM
+    // sub-partition to themselves (6 warps on 4) invert more matrices than the paired ones.
     const int64_t stride = int64_t(gridDim.x) * WPB;
+    int* jnext = reinterpret_cast<int*>(smem_raw + pad + WPB * (TILES_B + AUX_B));
+    if (threadIdx.x == 0) *jnext = WPB;
+    __syncthreads();
     int64_t b = int64_t(blockIdx.x) * WPB + warp;
 #ifdef HPDINV_DMMA_PROF
     long long prof_[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // wait F1d F2a F2b I1 I23 I4 S5 - -
@@ -343,7 +363,7 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, int64_t batch, double2* X, int64
     __syncwarp();
 
 #pragma unroll 1
-    for (unsigned it = 0; b < batch; b += stride, it++) {
+    for (unsigned it = 0; b < batch; it++) {
         const unsigned par = it & 1u;
         int inf = 0;
         // ========================================================== factorisation, panels up
@@ -524,11 +544,61 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, int64_t batch, double2* X, int64
 
         DM_PHASE(7);
         // ============================================ S5: store X, prefetch the next matrix
-        const int64_t bn = b + stride;
+        int jn = 0;
+        if (lane == 0) jn = atomicAdd(jnext, 1);
+        jn = __shfl_sync(0xffffffffu, jn, 0);
+        const int64_t bn = int64_t(jn / WPB) * stride + int64_t(blockIdx.x) * WPB + jn % WPB;
         double2* Xb = X + b * sXm;
         const double nan = qnan<double>();
         const int rr = lane >> 3, cc = lane & 7;
-        if (sXe == 1) {
+        if (xtma && !inf) {
+            // X through the tensor map (contiguous X): the 36 upper tiles are bulk-stored by the
+            // TMA engine straight from the swizzled tiles (one bulk group per tile row); the warp
+            // writes only the 28 lower tiles, as conjugate transposes.  Tile row I is reloaded
+            // for the next matrix once its group has been read out of shared memory.
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+                for (int I = 0; I < NTL; I++) {
+#pragma unroll
+                    for (int J = I; J < NTL; J++) tma_store_tile(&tmX, Tw + 64 * tidx(I, J), 16 * J, 8 * I, int(b));
+                    bulk_commit();
+                }
+            }
+            double2* Xl = Xb + (rr * N + cc);
+#pragma unroll
+            for (int I = 0; I < NTL; I++) {
+#pragma unroll
+                for (int J = I + 1; J < NTL; J++) {
+                    const double2* tl = Tw + 64 * tidx(I, J);
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const int ro = rr + 4 * h;
+                        double2 w = tl[sw(cc, ro)];                                 // (J, I) = conj^T
+                        w.y = negd(w.y);
+                        __stcs(Xl + ((8 * J + 4 * h) * N + 8 * I), w);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    switch (I) {                                   // groups of rows > I may still be pending
+                        case 0: bulk_wait_read<7>(); break;
+                        case 1: bulk_wait_read<6>(); break;
+                        case 2: bulk_wait_read<5>(); break;
+                        case 3: bulk_wait_read<4>(); break;
+                        case 4: bulk_wait_read<3>(); break;
+                        case 5: bulk_wait_read<2>(); break;
+                        case 6: bulk_wait_read<1>(); break;
+                        default: bulk_wait_read<0>(); break;
+                    }
+                    if (bn < batch) {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        load_row(Tw, &tmA, I, bn, &bar[I]);
+                    }
+                }
+            }
+        } else if (sXe == 1) {
             // contiguous X: every address is the lane base plus a compile-time offset
             double2* Xl = Xb + (rr * N + cc);
 #pragma unroll
@@ -578,8 +648,10 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, int64_t batch, double2* X, int64
             }
         }
         if (lane == 0) info[b] = inf;
+        b = bn;
         DM_PHASE(8);
     }
+    if (lane == 0) bulk_wait_all();                         // every bulk store of X has completed
 #ifdef HPDINV_DMMA_PROF
     DM_PHASE(8);
     if (lane == 0)

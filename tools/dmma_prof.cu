@@ -40,14 +40,14 @@ int main(int argc, char** argv) {
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     const int grid = int(batch < 148 * 6 ? (batch + 5) / 6 : 148);
     cudaFuncSetAttribute(k_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, dm::SMEM);
-    k_dmma<<<grid, dm::NT, dm::SMEM>>>(tm, batch, X, N * N, 1, info);
+    k_dmma<<<grid, dm::NT, dm::SMEM>>>(tm, tm, 0, batch, X, N * N, 1, info);
     unsigned long long z[32] = {0};
     cudaMemcpyToSymbol(dm::g_prof, z, sizeof(unsigned long long) * 16);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    k_dmma<<<grid, dm::NT, dm::SMEM>>>(tm, batch, X, N * N, 1, info);
+    k_dmma<<<grid, dm::NT, dm::SMEM>>>(tm, tm, 0, batch, X, N * N, 1, info);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
