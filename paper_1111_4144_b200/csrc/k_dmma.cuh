@@ -497,17 +497,27 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                 if (r <= 2 * q + 1) D[sw(2 * q + 1, r)] = make_double2(v.r1, v.i1);
                 __syncwarp();
                 const int j = lane & 7;
-                double2 xc[8];
+                double2 xc[8], rkc[8], rkn[8];
 #pragma unroll
-                for (int m = 0; m < 8; m++) xc[m] = make_double2(0.0, 0.0);
+                for (int m = 0; m < 8; m++) xc[m] = rkc[m] = rkn[m] = make_double2(0.0, 0.0);
+                double2 vn = D[sw(j, 7)];
 #pragma unroll
                 for (int k = 7; k >= 0; k--) {
                     const double ik = invs[K * 8 + k];
-                    // x_kj, j > k: -(1/r_kk)(V_kj + sum_{m>k} r_km x~_mj), two chains
-                    double2 s0 = D[sw(j, k)], s1 = make_double2(0.0, 0.0);
+                    // x_kj, j > k: -(1/r_kk)(V_kj + sum_{m>k} r_km x~_mj), two chains.  Row k of
+                    // R_KK and V_kj were loaded during step k+1 (neither changes in I4; slot
+                    // (j, k) is overwritten by the mirror only in this step)
+                    double2 s0 = vn, s1 = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int m = 7; m > k; m--) rkc[m] = rkn[m];
+                    if (k > 0) {
+                        vn = D[sw(j, k - 1)];
+#pragma unroll
+                        for (int m = 7; m > k - 1; m--) rkn[m] = D[sw(k - 1, m)];
+                    }
 #pragma unroll
                     for (int m = 7; m > k; m--) {
-                        const double2 rk = D[sw(k, m)];
+                        const double2 rk = rkc[m];
                         double2& sa = ((7 - m) & 1) ? s1 : s0;
                         sa.x = fma(rk.x, xc[m].x, sa.x); sa.x = fma(-rk.y, xc[m].y, sa.x);
                         sa.y = fma(rk.x, xc[m].y, sa.y); sa.y = fma(rk.y, xc[m].x, sa.y);
@@ -523,7 +533,7 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
 #pragma unroll
                         for (int m = 7; m > k; m--) {
                             const double2 g = D[sw(m, k)];                          // conj(x_km)
-                            const double2 rk = D[sw(k, m)];
+                            const double2 rk = rkc[m];
                             xc[m] = g;
                             double& pp = ((7 - m) & 1) ? p2 : p;
                             pp = fma(rk.x, g.x, pp);

@@ -192,6 +192,21 @@ def test_dmma_schedule_invariance():
     Xp, _ = hp.invert(Ap, "chol")
     torch.cuda.synchronize()
     assert torch.equal(Ain, X1) and torch.equal(Xp.contiguous(), X1)
+    # X written by per-lane stores instead of the TMA tensor store (interleaved X)
+    Xe = torch.full((64, 64, batch), float("nan"), dtype=A.dtype, device="cuda").permute(2, 0, 1)
+    hp.invert(A, "chol", X=Xe)
+    torch.cuda.synchronize()
+    assert torch.equal(Xe.contiguous(), X1)
+    # non-PD matrices in the stream (the NaN store path between TMA-stored neighbours)
+    An = A.clone()
+    bad = torch.tensor([0, 5, 887, 888, 1500, batch - 1], device="cuda")
+    An[bad, 40, 40] = -1.0
+    Xn, inf_n = hp.invert(An, "chol")
+    torch.cuda.synchronize()
+    ok = torch.ones(batch, dtype=torch.bool, device="cuda")
+    ok[bad] = False
+    assert bool((inf_n[bad] > 0).all()) and int(inf_n[ok].abs().sum()) == 0
+    assert bool(torch.isnan(Xn[bad]).all()) and torch.equal(Xn[ok], X1[ok])
 
 
 def test_kernel_names():
