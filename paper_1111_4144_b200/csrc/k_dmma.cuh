@@ -28,15 +28,19 @@
 //
 // Factor (eqs. 3-4), panels K = 0..7 (left-looking: the sums of eqs. 3-4 over k < 8K at once):
 //   F1  A_KJ -= sum_{P<K} R_PK^H R_PJ  for J >= K       (DMMA, accumulators start at A_KJ)
-//   F2a R_KK by the right-looking recursion of eqs. 3-4 on the accumulator registers (pivots
-//       and rows broadcast by shuffles); info = first k with !(t_k > 0)
-//   F2b R_KJ = R_KK^-H A_KJ, J > K: the forward substitution of eq. 4 on the accumulators
+//   F2a R_KK by the right-looking recursion of eqs. 3-4 on the accumulator registers (rows and
+//       pivots broadcast through the tile); the same row operations on I give E = R_KK^-H;
+//       info = first k with !(t_k > 0)
+//   F2b R_KJ = E A'_KJ, J > K  (DMMA; DESIGN reading R22: the panel solve as a product with the
+//       inverted 8 x 8 diagonal block)
 // Proposed inversion (eqs. 20-24), panels K = 7..0, T = K+1..7:
 //   I1  C_KJ = sum_{M in T} R_KM X~_MJ  for J in T    (DMMA; X~_MJ = X_JM^H read transposed)
-//   I2  x_kj = -(1/r_kk)(C_kj + sum_{m in K, m>k} r_km x_mj), k = 7..0 (registers, shuffles)
+//   I2  X_KJ = -E^H C_KJ                                (DMMA, R22)
 //   I3  V = sum_{J in T} R_KJ X_KJ^H                   (DMMA, X^H from the accumulators)
-//   I4  X_KK by the recursion of eq. 23 with V_kj added (lane j owns column j; the row
-//       gathered to the diagonal lane by shuffles is the mirror), x_kk real
+//   I4  X_KK by the recursion of eq. 23 with V_kj added (lane j owns column j; the mirror of
+//       each row goes through the tile's lower half to the diagonal lane), x_kk real
+// The complex products of F1, I1 and I2 take the three-multiplication form (C3, reading R24):
+// 3 real MMAs per complex k-step instead of 4.
 // S5  every tile to global memory, lower tiles as the conjugate transpose (bitwise mirror).
 #pragma once
 #include <cuda.h>
@@ -99,6 +103,29 @@ __device__ __forceinline__ void acc_load(CAcc& c, const double2* tl, int o0, int
 __device__ __forceinline__ void acc_store(const CAcc& c, double2* tl, int o0, int o1) {
     tl[o0] = make_double2(c.r0, c.i0);
     tl[o1] = make_double2(c.r1, c.i1);
+}
+
+// complex product-sum in the three-multiplication form (Gauss): for C += A B the accumulator
+// keeps P1 = sum ar br, P2 = sum ai bi and P3 = sum (ar + ai)(br + bi) -- three real MMAs per
+// k-step instead of four -- and Re C = P1 - P2, Im C = P3 - P1 - P2 at the end (reading R24)
+struct C3 { double p0, p1, q0, q1, s0, s1; };          // P1, P2, P3 for accumulator elements 0, 1
+__device__ __forceinline__ void c3zero(C3& c) { c.p0 = c.p1 = c.q0 = c.q1 = c.s0 = c.s1 = 0.0; }
+__device__ __forceinline__ void c3from(C3& c, const CAcc& x) {     // start from C = x
+    c.p0 = x.r0; c.p1 = x.r1; c.q0 = 0.0; c.q1 = 0.0; c.s0 = x.r0 + x.i0; c.s1 = x.r1 + x.i1;
+}
+__device__ __forceinline__ void c3mma(C3& c, double ar, double ai, double as, double br, double bi, double bs) {
+    dmma(c.p0, c.p1, ar, br);
+    dmma(c.q0, c.q1, ai, bi);
+    dmma(c.s0, c.s1, as, bs);
+}
+__device__ __forceinline__ void c3add(C3& c, const C3& d) {
+    c.p0 += d.p0; c.p1 += d.p1; c.q0 += d.q0; c.q1 += d.q1; c.s0 += d.s0; c.s1 += d.s1;
+}
+__device__ __forceinline__ CAcc c3val(const C3& c) {
+    CAcc x;
+    x.r0 = c.p0 - c.q0; x.r1 = c.p1 - c.q1;
+    x.i0 = (c.s0 - c.p0) - c.q0; x.i1 = (c.s1 - c.p1) - c.q1;
+    return x;
 }
 
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
@@ -192,8 +219,12 @@ __device__ __forceinline__ void dm_factor_off(double2* __restrict__ Tw, const Dm
     using namespace dm;
     constexpr int NT_ = NTL - 1 - K;
     CAcc a[NT_ > 0 ? NT_ : 1];
+    C3 a3[NT_ > 0 ? NT_ : 1];
 #pragma unroll
-    for (int u = 0; u < NT_; u++) acc_load(a[u], Tw + 64 * tidx(K, K + 1 + u), L.oa0, L.oa1);
+    for (int u = 0; u < NT_; u++) {
+        acc_load(a[u], Tw + 64 * tidx(K, K + 1 + u), L.oa0, L.oa1);
+        c3from(a3[u], a[u]);
+    }
     // k-steps (P, s) software-pipelined: the next step's fragments are loaded before this step's MMAs
     double2 w = Tw[64 * tidx(0, K) + L.ob0];
     double2 v[NT_ > 0 ? NT_ : 1];
@@ -209,11 +240,9 @@ __device__ __forceinline__ void dm_factor_off(double2* __restrict__ Tw, const Dm
 #pragma unroll
             for (int u = 0; u < NT_; u++) vn[u] = Tw[64 * tidx(Pn, K + 1 + u) + obn];   // B = R_PJ
         }
-        const double ar = negd(w.x), ai = w.y, nai = negd(w.y);
+        const double ar = negd(w.x), ai = w.y, as = w.y - w.x;
 #pragma unroll
-        for (int u = 0; u < NT_; u++) cmma_h1(a[u], ar, v[u].x, v[u].y);
-#pragma unroll
-        for (int u = 0; u < NT_; u++) cmma_h2(a[u], ai, nai, v[u].x, v[u].y);
+        for (int u = 0; u < NT_; u++) c3mma(a3[u], ar, ai, as, v[u].x, v[u].y, v[u].x + v[u].y);
         (void)P;
         w = wn;
 #pragma unroll
@@ -221,7 +250,10 @@ __device__ __forceinline__ void dm_factor_off(double2* __restrict__ Tw, const Dm
     }
     // A' through its own tile, read back as the B operand of E A'
 #pragma unroll
-    for (int u = 0; u < NT_; u++) acc_store(a[u], Tw + 64 * tidx(K, K + 1 + u), L.oa0, L.oa1);
+    for (int u = 0; u < NT_; u++) {
+        a[u] = c3val(a3[u]);
+        acc_store(a[u], Tw + 64 * tidx(K, K + 1 + u), L.oa0, L.oa1);
+    }
     __syncwarp();
     double2 b0[NT_ > 0 ? NT_ : 1], b1[NT_ > 0 ? NT_ : 1];
 #pragma unroll
@@ -230,6 +262,8 @@ __device__ __forceinline__ void dm_factor_off(double2* __restrict__ Tw, const Dm
         b1[u] = Tw[64 * tidx(K, K + 1 + u) + L.ob1];
     }
     __syncwarp();
+    // (four-multiplication form here: the three-multiplication one measured slower on this
+    //  latency-bound 2-k-step product, 19.8 vs 18.7 ms at cfg4)
     const double ne0 = negd(e.i0), ne1 = negd(e.i1);
 #pragma unroll
     for (int u = 0; u < NT_; u++) {
@@ -250,8 +284,9 @@ __device__ __forceinline__ void dm_invert_off(double2* Tw, const DmLane& L, CAcc
     constexpr int NT_ = NTL - 1 - K;
     constexpr int M0 = K + 1;
     CAcc a[NT_];
+    C3 a3[NT_];
 #pragma unroll
-    for (int u = 0; u < NT_; u++) czero(a[u]);
+    for (int u = 0; u < NT_; u++) c3zero(a3[u]);
     // k-steps (m, s) software-pipelined: the next step's fragments are loaded before this step's MMAs
     auto ldx = [&](int m, int s, int u) -> double2 {
         double2 x;
@@ -272,15 +307,15 @@ __device__ __forceinline__ void dm_invert_off(double2* Tw, const DmLane& L, CAcc
 #pragma unroll
             for (int u = 0; u < NT_; u++) xn[u] = ldx(mn, sn, u);
         }
-        const double nwi = negd(w.y);
+        const double ws = w.x + w.y;
 #pragma unroll
-        for (int u = 0; u < NT_; u++) cmma_h1(a[u], w.x, x[u].x, x[u].y);
-#pragma unroll
-        for (int u = 0; u < NT_; u++) cmma_h2(a[u], w.y, nwi, x[u].x, x[u].y);
+        for (int u = 0; u < NT_; u++) c3mma(a3[u], w.x, w.y, ws, x[u].x, x[u].y, x[u].x + x[u].y);
         w = wn;
 #pragma unroll
         for (int u = 0; u < NT_; u++) x[u] = xn[u];
     }
+#pragma unroll
+    for (int u = 0; u < NT_; u++) a[u] = c3val(a3[u]);
     const double2* tKK = Tw + 64 * tidx(K, K);
     double ra0, ia0, ra1, ia1;                                          // A = -R_KK^-1
     {
@@ -298,16 +333,20 @@ __device__ __forceinline__ void dm_invert_off(double2* Tw, const DmLane& L, CAcc
         acc_store(a[u], tKJ, L.oa0, L.oa1);                             // C_KJ
     }
     __syncwarp();
+    // I2 in the three-multiplication form; I3 (B straight from I2's accumulators) in the four-
+    // multiplication form, which measured faster there (shorter chain, fewer registers)
     CAcc v2;
     czero(v2);
-    const double nia0 = negd(ia0), nia1 = negd(ia1);
+    const double as0 = ra0 + ia0, as1 = ra1 + ia1;
 #pragma unroll
     for (int u = 0; u < NT_; u++) {
         const double2* tKJ = Tw + 64 * tidx(K, K + 1 + u);
         const double2 b0 = tKJ[L.ob0], b1 = tKJ[L.ob1];
-        czero(a[u]);
-        cmma(a[u], ra0, ia0, nia0, b0.x, b0.y);
-        cmma(a[u], ra1, ia1, nia1, b1.x, b1.y);
+        c3zero(a3[u]);
+        c3mma(a3[u], ra0, ia0, as0, b0.x, b0.y, b0.x + b0.y);
+        c3mma(a3[u], ra1, ia1, as1, b1.x, b1.y, b1.x + b1.y);
+        a[u] = c3val(a3[u]);                                            // X_KJ
+        // V += R_KJ X_KJ^H: B = conj(X_KJ) straight from the accumulators
         CAcc& vv = (u & 1) ? v2 : v;
         cmma(vv, u0[u].x, u0[u].y, negd(u0[u].y), a[u].r0, negd(a[u].i0));
         cmma(vv, u1[u].x, u1[u].y, negd(u1[u].y), a[u].r1, negd(a[u].i1));
@@ -376,34 +415,35 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             // ---- F1 on the diagonal tile: A_KK -= sum_{P<K} R_PK^H R_PK
             // four accumulators (P even / odd x k-step s) and split MMA halves: the dependent MMA
             // chain of the diagonal tile is a quarter as long
-            CAcc d, d1, d2, d3;
+            CAcc d;
             acc_load(d, tKK, oa0, oa1);
-            czero(d1);
-            czero(d2);
-            czero(d3);
+            C3 d0, d1, d2, d3;
+            c3from(d0, d);
+            c3zero(d1);
+            c3zero(d2);
+            c3zero(d3);
             {
+                // A = -conj(R_PK)^T = (-x, y), B = R_PK = (x, y): (ar + ai)(br + bi) = y^2 - x^2
                 int P = 0;
 #pragma unroll 1
                 for (; P + 1 < K; P += 2) {
-                    const double2 u0 = TILE(P, K)[ob0], u1 = TILE(P, K)[ob1];       // A = -conj(R_PK)^T, B = R_PK
+                    const double2 u0 = TILE(P, K)[ob0], u1 = TILE(P, K)[ob1];
                     const double2 w0 = TILE(P + 1, K)[ob0], w1 = TILE(P + 1, K)[ob1];
-                    cmma_h1(d, negd(u0.x), u0.x, u0.y);
-                    cmma_h1(d1, negd(u1.x), u1.x, u1.y);
-                    cmma_h1(d2, negd(w0.x), w0.x, w0.y);
-                    cmma_h1(d3, negd(w1.x), w1.x, w1.y);
-                    cmma_h2(d, u0.y, negd(u0.y), u0.x, u0.y);
-                    cmma_h2(d1, u1.y, negd(u1.y), u1.x, u1.y);
-                    cmma_h2(d2, w0.y, negd(w0.y), w0.x, w0.y);
-                    cmma_h2(d3, w1.y, negd(w1.y), w1.x, w1.y);
+                    c3mma(d0, negd(u0.x), u0.y, u0.y - u0.x, u0.x, u0.y, u0.x + u0.y);
+                    c3mma(d1, negd(u1.x), u1.y, u1.y - u1.x, u1.x, u1.y, u1.x + u1.y);
+                    c3mma(d2, negd(w0.x), w0.y, w0.y - w0.x, w0.x, w0.y, w0.x + w0.y);
+                    c3mma(d3, negd(w1.x), w1.y, w1.y - w1.x, w1.x, w1.y, w1.x + w1.y);
                 }
                 if (P < K) {
                     const double2 u0 = TILE(P, K)[ob0], u1 = TILE(P, K)[ob1];
-                    cmma(d, negd(u0.x), u0.y, negd(u0.y), u0.x, u0.y);
-                    cmma(d1, negd(u1.x), u1.y, negd(u1.y), u1.x, u1.y);
+                    c3mma(d0, negd(u0.x), u0.y, u0.y - u0.x, u0.x, u0.y, u0.x + u0.y);
+                    c3mma(d1, negd(u1.x), u1.y, u1.y - u1.x, u1.x, u1.y, u1.x + u1.y);
                 }
             }
-            d.r0 += (d1.r0 + d2.r0) + d3.r0; d.r1 += (d1.r1 + d2.r1) + d3.r1;
-            d.i0 += (d1.i0 + d2.i0) + d3.i0; d.i1 += (d1.i1 + d2.i1) + d3.i1;
+            c3add(d1, d2);
+            c3add(d1, d3);
+            c3add(d0, d1);
+            d = c3val(d0);
             DM_PHASE(2);
             // ---- F2a: R_KK by the right-looking recursion of eqs. 3-4 on the accumulators, and
             //      E = R_KK^-H (the same row operations applied to I), for the panel solves.
