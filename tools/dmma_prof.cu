@@ -38,16 +38,19 @@ int main(int argc, char** argv) {
     const cuuint32_t box[3] = {16, 8, 1}, es[3] = {1, 1, 1};
     enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, A, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUtensorMap tx;                                   // X by TMA bulk stores, as the library does
+    enc(&tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, X, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     const int grid = int(batch < 148 * 6 ? (batch + 5) / 6 : 148);
     cudaFuncSetAttribute(k_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, dm::SMEM);
-    k_dmma<<<grid, dm::NT, dm::SMEM>>>(tm, tm, 0, batch, X, N * N, 1, info);
+    k_dmma<<<grid, dm::NT, dm::SMEM>>>(tm, tx, 1, batch, X, N * N, 1, info);
     unsigned long long z[32] = {0};
     cudaMemcpyToSymbol(dm::g_prof, z, sizeof(unsigned long long) * 16);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    k_dmma<<<grid, dm::NT, dm::SMEM>>>(tm, tm, 0, batch, X, N * N, 1, info);
+    k_dmma<<<grid, dm::NT, dm::SMEM>>>(tm, tx, 1, batch, X, N * N, 1, info);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
