@@ -35,6 +35,25 @@ static int launch_grp_t(const LaunchArgs& a) {
     // n >= 9 that fits in device memory does)
     if (!grp_strides_ok(a.sAe, a.sXe, sizeof(cplx<T>))) fn = nullptr;
     if (!fn) return kNoKernel;
+#ifndef HPDINV_GRP_NO_STAGE
+    // staged global I/O (bulk copies of whole CTA plane segments, k_grp.cuh STG): interleaved A
+    // and X with even plane strides and 16-byte aligned bases, n <= 16
+    const bool stg = a.n <= 16 && a.sAm == 1 && a.sXm == 1 && a.sAe % 2 == 0 && a.sXe % 2 == 0 &&
+                     (reinterpret_cast<uintptr_t>(a.A) & 15) == 0 && (reinterpret_cast<uintptr_t>(a.X) & 15) == 0;
+    if (stg) {
+        switch (a.n) {
+#define HPDINV_GRP_STG(NN)                                   \
+            case NN:                                         \
+                fn = k_grp<T, NN, 4, LDL, true>;             \
+                smem = GrpShape<T, NN, 4>::smem_bytes_staged; \
+                break;
+            HPDINV_GRP_STG(9) HPDINV_GRP_STG(10) HPDINV_GRP_STG(11) HPDINV_GRP_STG(12)
+            HPDINV_GRP_STG(13) HPDINV_GRP_STG(14) HPDINV_GRP_STG(15) HPDINV_GRP_STG(16)
+#undef HPDINV_GRP_STG
+            default: break;
+        }
+    }
+#endif
     cudaError_t e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
     if (e != cudaSuccess) return int(e);
     const int64_t blocks = (a.batch + mpc - 1) / mpc;

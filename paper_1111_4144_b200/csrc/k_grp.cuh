@@ -73,6 +73,20 @@ struct GrpShape {
     static constexpr int raw_bytes = (RSZ + 2 * RB) * ESZ + ((N * int(sizeof(T)) + 15) / 16) * 16;
     static constexpr int MSTR_B = ((raw_bytes + 127) / 128) * 128 + 16;
     static constexpr size_t smem_bytes = size_t(MPC) * MSTR_B;
+    // ---- staged global I/O (interleaved SoA, the CTA's MPC matrices contiguous in every plane):
+    // one element plane of the CTA is a contiguous MPC*ESZ-byte segment in global memory, moved
+    // by one cp.async.bulk; in shared memory the segments sit SPS bytes apart (= 32 mod 128): a
+    // half-warp of 8-byte accesses is 4 matrices x the G = 4 consecutive planes of one warp
+    // instruction, 4 disjoint 32-byte bank ranges, so a 256-byte LDS/STS is two wavefronts.  The staging area overlaps the row stores: the upper
+    // planes of A before S2, then X in two halves of rows after S4.
+    static constexpr int SPS = MPC * ESZ + 32;
+    static constexpr int NUP = N * (N + 1) / 2;         // upper planes of A
+    static constexpr int HROWS = (N + 1) / 2;           // X rows per store half
+    __host__ __device__ static constexpr int pidx(int l, int j) { return l * N - l * (l - 1) / 2 + (j - l); }
+    static constexpr size_t stage_bytes = size_t(NUP) * SPS > size_t(HROWS) * N * SPS ? size_t(NUP) * SPS
+                                                                                        : size_t(HROWS) * N * SPS;
+    static constexpr size_t region_bytes = stage_bytes > smem_bytes ? stage_bytes : smem_bytes;
+    static constexpr size_t smem_bytes_staged = region_bytes + 16;   // + the mbarrier
 };
 
 namespace grp {
@@ -93,21 +107,46 @@ __device__ __forceinline__ void lds_pair(const cplx<T>* p, int o, cplx<T>& e0, c
         e1 = e0;
     }
 }
+// bulk copies (async proxy: no LSU request, no L1 tag or data-stage wavefront per sector)
+__device__ __forceinline__ uint32_t s32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(s32(dst)), "l"(src), "r"(bytes), "r"(s32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(dst), "r"(s32(src)), "r"(bytes) : "memory");
+}
 }  // namespace grp
 
 // S1 + S2 of a lane group (shared by the inversion k_grp and the solve k_grp_solve): lane q
 // loads the upper part of its columns j = q + G*s and runs the right-looking factorisation with
 // the packed row store Rs; returns info.  See k_grp for the design notes.
-template <typename T, int N, int GG, bool LDL>
+template <typename T, int N, int GG, bool LDL, bool STG = false>
 __device__ __forceinline__ int grp_factor(cplx<T> (&col)[GrpShape<T, N, GG>::C][N], const cplx<T>* __restrict__ Am,
-                                          int64_t sAe, int q, cplx<T>* Rs, T* invs) {
+                                          int64_t sAe, int q, cplx<T>* Rs, T* invs,
+                                          const unsigned char* stq = nullptr) {
     using Sh = GrpShape<T, N, GG>;
     using V = cplx<T>;
     constexpr int G = Sh::G, C = Sh::C, P = Sh::P;
     constexpr unsigned FULL = 0xffffffffu;
     // ---------------------------------------------------------------- S1: load columns
     // (entries below the diagonal of a column are dead storage; Im a_jj is never read)
-    {
+    if (STG && stq) {
+        // from the staged upper planes: element (l, j = q + G*s) at stq + pidx(l, G*s) * SPS
+        // (stq = staging base + this lane's matrix slot + q planes)
+#pragma unroll
+        for (int s = 0; s < C; s++) {
+            const int j = q + G * s;
+#pragma unroll
+            for (int l = 0; l < N; l++) {
+                col[s][l] = czero<T>();
+                if (l <= G * s + G - 1 && l <= j && j < N)
+                    col[s][l] = *reinterpret_cast<const V*>(stq + Sh::pidx(l, G * s) * Sh::SPS);
+            }
+        }
+        __syncthreads();                                  // the staging area becomes row stores
+    } else {
         // element (l, j = q + G*s): lane base + (l*n + G*s) * plane stride; the plane stride in
         // bytes is < 2^32 (checked by the launcher), so each address is one IMAD.WIDE
         const char* Ab = reinterpret_cast<const char*>(Am + q * sAe);
@@ -185,7 +224,11 @@ __device__ __forceinline__ int grp_factor(cplx<T> (&col)[GrpShape<T, N, GG>::C][
     return inf;
 }
 
-template <typename T, int N, int GG, bool LDL>
+// STG: staged global I/O (interleaved A and X, sAm = sXm = 1, even plane strides, 16-byte
+// aligned bases -- checked by the launcher): a CTA holding MPC whole matrices moves its NUP
+// upper planes of A and its n^2 planes of X as bulk copies of MPC*ESZ bytes each through the
+// shared-memory staging area (GrpShape::SPS); a partial last CTA takes the per-lane path.
+template <typename T, int N, int GG, bool LDL, bool STG = false>
 __global__ void __launch_bounds__(GrpShape<T, N, GG>::THREADS, GrpShape<T, N, GG>::MIN_BLOCKS)
 k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
       cplx<T>* X, int64_t sXm, int64_t sXe, int32_t* __restrict__ info)
@@ -199,7 +242,8 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int q = lane & (G - 1), g = lane / G;
     const int mloc = warp * Sh::MPW + g;
-    int64_t b = int64_t(blockIdx.x) * Sh::MPC + mloc;
+    const int64_t b0 = int64_t(blockIdx.x) * Sh::MPC;
+    int64_t b = b0 + mloc;
     const bool valid = b < batch;
     b = valid ? b : batch - 1;                        // the tail recomputes (never stores) the last matrix
     unsigned char* mbase = smem_raw + size_t(mloc) * Sh::MSTR_B;
@@ -207,8 +251,39 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
     V* rowbuf0 = Rs + Sh::RSZ;                                        // X row k (k odd: + RB)
     T* invs = reinterpret_cast<T*>(rowbuf0 + 2 * Sh::RB);             // 1/r_kk or 1/d_k
 
+    // staged: the whole CTA is in the batch (uniform per CTA)
+    const bool full = STG && b0 + Sh::MPC <= batch;
+    const unsigned char* stq = nullptr;
+#ifdef HPDINV_GRP_STAGE_LOADS
+    if (STG && full) {
+        uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + Sh::region_bytes);
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(grp::s32(bar)) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (warp == 0) {
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                             ::"r"(grp::s32(bar)), "r"(unsigned(Sh::NUP * Sh::MPC * Sh::ESZ)) : "memory");
+            __syncwarp();
+            for (int p = lane; p < Sh::NUP; p += 32) {
+                int l = 0, r = p;
+                while (r >= N - l) { r -= N - l; l++; }
+                grp::bulk_g2s(smem_raw + p * Sh::SPS, A + b0 + int64_t(l * N + l + r) * sAe,
+                              unsigned(Sh::MPC * Sh::ESZ), bar);
+            }
+        }
+        asm volatile(
+            "{\n.reg .pred p;\nWAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+            "@!p bra WAIT_%=;\n}\n" ::"r"(grp::s32(bar)) : "memory");
+        stq = smem_raw + mloc * Sh::ESZ + q * Sh::SPS;
+    }
+#endif
+
     V col[C][N];
-    int inf = grp_factor<T, N, GG, LDL>(col, A + b * sAm, sAe, q, Rs, invs);
+    int inf = grp_factor<T, N, GG, LDL, STG>(col, A + b * sAm, sAe, q, Rs, invs, stq);
 
     // ------------------------------------------------ S3/S4: proposed inversion, rows k = n..1
 #pragma unroll
@@ -275,7 +350,39 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
     }
 
     // ------------------------------------------------------------------ S5: mirror + store
-    if (valid) {
+    if (STG && full) {
+        // X through the staging area in two halves of rows: every lane writes its columns'
+        // entries (m, j) of the half into plane m*n + j of its matrix slot, then each thread
+        // bulk-stores planes of the half (MPC*ESZ bytes each, contiguous in X)
+        __syncthreads();                                   // every row store / row buffer is dead
+        unsigned char* stw = smem_raw + mloc * Sh::ESZ + q * Sh::SPS;
+        const T nan = qnan<T>();
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            constexpr int H = Sh::HROWS;
+            const int m0 = h * H;
+#pragma unroll
+            for (int s = 0; s < C; s++) {
+                if (q + G * s < N) {
+#pragma unroll
+                    for (int m = 0; m < H; m++)
+                        if (m0 + m < N)
+                            *reinterpret_cast<V*>(stw + ((m * N) + G * s) * Sh::SPS) =
+                                inf ? mk<T>(nan, nan) : col[s][m0 + m];
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            const int np = (N - m0 < H ? N - m0 : H) * N;
+            for (int p = threadIdx.x; p < np; p += Sh::THREADS)
+                grp::bulk_s2g(X + b0 + int64_t(m0 * N + p) * sXe, smem_raw + p * Sh::SPS,
+                              unsigned(Sh::MPC * Sh::ESZ));
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            if (h == 0) __syncthreads();                   // the second half reuses the area
+        }
+        if (q == 0) info[b] = inf;
+    } else if (valid) {
         // (storing each row as soon as it is final, inside S4, measured slower: 4.5 vs 4.1 ms cfg3)
         // every entry (m, j) is written once, by the owner of column j; a flagged matrix is
         // NaN-filled in the same store
