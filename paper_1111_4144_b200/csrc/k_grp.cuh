@@ -73,15 +73,24 @@ struct GrpShape {
     static constexpr int raw_bytes = (RSZ + 2 * RB) * ESZ + ((N * int(sizeof(T)) + 15) / 16) * 16;
     static constexpr int MSTR_B = ((raw_bytes + 127) / 128) * 128 + 16;
     static constexpr size_t smem_bytes = size_t(MPC) * MSTR_B;
+    // matrix -> row-store slot: with 8 groups per warp, group g sits at 16-byte bank quad
+    // 2*(g%4) + g/4 (mod 8), so the 32-byte runs that the 4 groups of a half-warp write into
+    // their row stores are disjoint (one wavefront per half-warp instead of two) while the 8
+    // groups' 16-byte row broadcasts still hit 8 distinct quads
+    __host__ __device__ static constexpr int slot(int mloc) {
+        return MPW == 8 ? (mloc & ~7) + 2 * (mloc & 3) + ((mloc >> 2) & 1) : mloc;
+    }
     // ---- staged global I/O (interleaved SoA, the CTA's MPC matrices contiguous in every plane):
     // one element plane of the CTA is a contiguous MPC*ESZ-byte segment in global memory, moved
     // by one cp.async.bulk; in shared memory the segments sit SPS bytes apart (= 32 mod 128): a
     // half-warp of 8-byte accesses is 4 matrices x the G = 4 consecutive planes of one warp
     // instruction, 4 disjoint 32-byte bank ranges, so a 256-byte LDS/STS is two wavefronts.  The staging area overlaps the row stores: the upper
-    // planes of A before S2, then X in two halves of rows after S4.
+    // planes of A before S2, then X (whole, or in two halves of rows) after S4.
     static constexpr int SPS = MPC * ESZ + 32;
     static constexpr int NUP = N * (N + 1) / 2;         // upper planes of A
-    static constexpr int HROWS = (N + 1) / 2;           // X rows per store half
+    // X rows per store pass: two halves (the whole of X at once, 74 KB per CTA, leaves L1 almost
+    // no capacity next to three CTAs' shared memory: cfg3 3.65 -> 4.49 ms)
+    static constexpr int HROWS = (N + 1) / 2;
     __host__ __device__ static constexpr int pidx(int l, int j) { return l * N - l * (l - 1) / 2 + (j - l); }
     static constexpr size_t stage_bytes = size_t(NUP) * SPS > size_t(HROWS) * N * SPS ? size_t(NUP) * SPS
                                                                                         : size_t(HROWS) * N * SPS;
@@ -246,7 +255,7 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
     int64_t b = b0 + mloc;
     const bool valid = b < batch;
     b = valid ? b : batch - 1;                        // the tail recomputes (never stores) the last matrix
-    unsigned char* mbase = smem_raw + size_t(mloc) * Sh::MSTR_B;
+    unsigned char* mbase = smem_raw + size_t(Sh::slot(mloc)) * Sh::MSTR_B;
     V* Rs = reinterpret_cast<V*>(mbase);                              // packed R rows
     V* rowbuf0 = Rs + Sh::RSZ;                                        // X row k (k odd: + RB)
     T* invs = reinterpret_cast<T*>(rowbuf0 + 2 * Sh::RB);             // 1/r_kk or 1/d_k
@@ -351,14 +360,14 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
 
     // ------------------------------------------------------------------ S5: mirror + store
     if (STG && full) {
-        // X through the staging area in two halves of rows: every lane writes its columns'
+        // X through the staging area (whole, or in two halves of rows): every lane writes its columns
         // entries (m, j) of the half into plane m*n + j of its matrix slot, then each thread
         // bulk-stores planes of the half (MPC*ESZ bytes each, contiguous in X)
         __syncthreads();                                   // every row store / row buffer is dead
         unsigned char* stw = smem_raw + mloc * Sh::ESZ + q * Sh::SPS;
         const T nan = qnan<T>();
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
+        for (int h = 0; h < (N + Sh::HROWS - 1) / Sh::HROWS; h++) {
             constexpr int H = Sh::HROWS;
             const int m0 = h * H;
 #pragma unroll
@@ -379,7 +388,7 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
                               unsigned(Sh::MPC * Sh::ESZ));
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            if (h == 0) __syncthreads();                   // the second half reuses the area
+            if (m0 + H < N) __syncthreads();               // the second half reuses the area
         }
         if (q == 0) info[b] = inf;
     } else if (valid) {
@@ -431,7 +440,7 @@ k_grp_solve(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t s
     int64_t b = int64_t(blockIdx.x) * Sh::MPC + mloc;
     const bool valid = b < batch;
     b = valid ? b : batch - 1;                        // the tail recomputes (never stores) the last system
-    unsigned char* mbase = smem_raw + size_t(mloc) * Sh::MSTR_B;
+    unsigned char* mbase = smem_raw + size_t(Sh::slot(mloc)) * Sh::MSTR_B;
     V* Rs = reinterpret_cast<V*>(mbase);
     T* invs = reinterpret_cast<T*>(Rs + Sh::RSZ + 2 * Sh::RB);
 
