@@ -212,3 +212,30 @@ def test_dmma_schedule_invariance():
 def test_kernel_names():
     assert hp.kernel_name("chol", torch.complex64, 1 << 20, 8, (1, 1 << 20)) is not None
     assert hp.kernel_name("chol", torch.complex64, 8, 65) is None
+
+
+@pytest.mark.parametrize("n", [9, 13, 16])
+@pytest.mark.parametrize("method", ["chol", "ldl"])
+def test_grp_staged_io_invariance(n, method):
+    """k_grp's staged global I/O (bulk copies of whole CTA plane segments through shared memory,
+    taken for interleaved A/X with even plane strides and 16-byte aligned bases) and its
+    per-lane path (odd plane stride, or an 8-byte aligned X) give bitwise the same X and info,
+    full CTAs, a ragged last CTA and NaN-filled flagged matrices included."""
+    cfg = wl.Config(97, n, torch.complex64, 0, method, "soa", "bbh", float(n), 0.1)
+    batch = 5 * 32 + 19
+    A = wl.generate(cfg, 0, batch, device="cuda").clone()
+    A[7, n // 2, n // 2] = -1.0                      # flagged inside a full CTA
+    A[batch - 3, 0, 0] = -2.0                        # flagged in the ragged CTA
+    Xs, is_, _ = gc.run_gpu(A, method, "soa")                    # staged (ld = batch, even)
+    Xp, ip, _ = gc.run_gpu(A, method, "soa", ld=batch + 1)       # odd plane stride: per-lane path
+    assert np.array_equal(is_, ip) and is_[7] != 0 and is_[batch - 3] == 1
+    assert np.array_equal(Xs.view(np.float64), Xp.view(np.float64), equal_nan=True)
+    # X base 8-byte aligned only: per-lane stores
+    _, view = wl.to_layout(A, "soa")
+    store = torch.empty(n * n * batch + 1, dtype=A.dtype, device="cuda")
+    X = torch.as_strided(store[1:], view.shape, view.stride())
+    X, info = hp.invert(view, method, X=X)
+    torch.cuda.synchronize()
+    Xm = X.contiguous().cpu().to(torch.complex128).numpy()
+    assert np.array_equal(info.cpu().numpy(), is_)
+    assert np.array_equal(Xm.view(np.float64), Xs.view(np.float64), equal_nan=True)
