@@ -23,8 +23,11 @@ static int launch_nh_t(const LaunchArgs& a) {
     const V* D = static_cast<const V*>(a.A);
     V* Y = static_cast<V*>(a.X);
     if (fn) {
+        const size_t smem = size_t(a.n) * a.n * sizeof(V) * kRegThreads;   // D, one column per thread
+        cudaError_t e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
+        if (e != cudaSuccess) return int(e);
         const int64_t blocks = (a.batch + kRegThreads - 1) / kRegThreads;
-        fn<<<unsigned(blocks), kRegThreads, 0, a.stream>>>(a.batch, D, a.sAm, a.sAe, Y, a.sXm, a.sXe, a.info);
+        fn<<<unsigned(blocks), kRegThreads, smem, a.stream>>>(a.batch, D, a.sAm, a.sAe, Y, a.sXm, a.sXe, a.info);
         return int(cudaGetLastError());
     }
     auto gfn = k_nh_gen<T>;

@@ -6,8 +6,8 @@
 //   k_nh_reg: one matrix per thread (c64 n <= 8, c128 n <= 6).  A's packed upper triangle is
 //             accumulated column by column of D (a_ij += d_ip conj(d_jp)), so only one column
 //             of D and the triangle are live; D^-1 is formed row by row, (D^-1)_ij =
-//             sum_p conj(d_pi) x_pj, re-reading column i of D (an L2 hit: the same thread read
-//             it moments before).
+//             sum_p conj(d_pi) x_pj, re-reading column i of D from the thread's shared-memory
+//             copy (written during the first pass).
 //   k_nh_gen: one matrix per CTA in shared memory, any n <= 64 (correctness path).
 // info: the Cholesky info of A = DD* (0 <=> D numerically nonsingular); D^-1 NaN when flagged.
 #pragma once
@@ -26,6 +26,10 @@ k_nh_reg(int64_t batch, const cplx<T>* __restrict__ D, int64_t sDm, int64_t sDe,
     const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (b >= batch) return;
     const V* Db = D + b * sDm;
+    // D as read in the first pass, kept for the second in this thread's shared-memory column
+    // (element e at Ds[e * blockDim.x]: a warp's 8- or 16-byte accesses are conflict-free)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V* Ds = reinterpret_cast<V*>(smem_raw) + threadIdx.x;
 
     V r[NU];
 #pragma unroll
@@ -33,13 +37,21 @@ k_nh_reg(int64_t batch, const cplx<T>* __restrict__ D, int64_t sDm, int64_t sDe,
     {                                                   // A = D D*, p ascending (column p+1
         V c[N];                                         // fetched during the update with p)
 #pragma unroll
-        for (int i = 0; i < N; i++) c[i] = __ldg(Db + int64_t(i * N) * sDe);
+        for (int i = 0; i < N; i++) {
+            c[i] = __ldg(Db + int64_t(i * N) * sDe);
+            Ds[(i * N) * kRegThreads] = c[i];
+        }
 #pragma unroll
         for (int p = 0; p < N; p++) {
             V cn[N];
             const int p1 = p + 1 < N ? p + 1 : p;
+            if (p + 1 < N) {
 #pragma unroll
-            for (int i = 0; i < N; i++) cn[i] = __ldg(Db + int64_t(i * N + p1) * sDe);
+                for (int i = 0; i < N; i++) {
+                    cn[i] = __ldg(Db + int64_t(i * N + p1) * sDe);
+                    Ds[(i * N + p1) * kRegThreads] = cn[i];
+                }
+            }
 #pragma unroll
             for (int i = 0; i < N; i++)
 #pragma unroll
@@ -58,17 +70,18 @@ k_nh_reg(int64_t batch, const cplx<T>* __restrict__ D, int64_t sDm, int64_t sDe,
 
     V* Yb = Y + b * sYm;
     const T nan = qnan<T>();
-    // rows of D^-1 = D* X, i ascending; column i+1 of D is fetched while row i is formed (fully
-    // unrolled: 0.37 -> 0.34 ms at cfg7 against rolled loops, despite 255 registers)
+    // rows of D^-1 = D* X, i ascending; column i+1 of D is read (shared memory) while row i is
+    // formed (fully unrolled: 0.37 -> 0.34 ms at cfg7 against rolled loops, despite 255 registers;
+    // re-reading D from L2 instead of shared memory: 0.34 ms)
     V c[N];
 #pragma unroll
-    for (int p = 0; p < N; p++) c[p] = __ldg(Db + int64_t(p * N) * sDe);               // d_p0
+    for (int p = 0; p < N; p++) c[p] = Ds[(p * N) * kRegThreads];                     // d_p0
 #pragma unroll
     for (int i = 0; i < N; i++) {
         V cn[N];
         const int i1 = i + 1 < N ? i + 1 : i;
 #pragma unroll
-        for (int p = 0; p < N; p++) cn[p] = __ldg(Db + int64_t(p * N + i1) * sDe);
+        for (int p = 0; p < N; p++) cn[p] = Ds[(p * N + i1) * kRegThreads];
 #pragma unroll
         for (int j = 0; j < N; j++) {
             V s = czero<T>();
