@@ -55,7 +55,7 @@ constexpr int NTILE = NTL * (NTL + 1) / 2;           // 36 upper tiles
 constexpr int WPB = 6;                               // warps (matrices) per CTA, one CTA per SM
 constexpr int NT = 32 * WPB;
 constexpr int TILES_B = NTILE * 1024;                // 36 tiles per warp
-constexpr int AUX_B = 64 * 8 + 8 * 8;                // per warp: 1/r_kk (64 doubles), 8 mbarriers
+constexpr int AUX_B = 64 * 8 + 8 * 8 + 8 * 8;        // per warp: 1/r_kk (64 doubles), 8 mbarriers, 8 I4 partials
 constexpr int SMEM = WPB * (TILES_B + AUX_B) + 16 + 1024; // + the CTA's matrix counter + alignment slack (TMA 128B swizzle)
 
 __host__ __device__ constexpr int tidx(int I, int J) { return I * NTL - I * (I - 1) / 2 + (J - I); }
@@ -371,6 +371,7 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     double2* Tw = reinterpret_cast<double2*>(smem_raw + pad + warp * TILES_B);      // this warp's tiles
     double* invs = reinterpret_cast<double*>(smem_raw + pad + WPB * TILES_B + warp * AUX_B);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + pad + WPB * TILES_B + warp * AUX_B + 64 * 8);
+    double* tpart = reinterpret_cast<double*>(smem_raw + pad + WPB * TILES_B + warp * AUX_B + 64 * 8 + 8 * 8);
 #define TILE(I, J) (Tw + rowbase(I) + 64 * (J))
 
     const int r = lane >> 2, q = lane & 3;             // accumulator row, column pair
@@ -541,6 +542,9 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
 #pragma unroll
                 for (int m = 0; m < 8; m++) xc[m] = rkc[m] = rkn[m] = make_double2(0.0, 0.0);
                 double2 vn = D[sw(j, 7)];
+#ifndef HPDINV_DMMA_I4_CHAIN
+                double2 rjn = D[sw(7, j)];                  // r_kj of the next step (upper half: R_KK)
+#endif
 #pragma unroll
                 for (int k = 7; k >= 0; k--) {
                     const double ik = invs[K * 8 + k];
@@ -550,6 +554,10 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                     double2 s0 = vn, s1 = make_double2(0.0, 0.0);
 #pragma unroll
                     for (int m = 7; m > k; m--) rkc[m] = rkn[m];
+#ifndef HPDINV_DMMA_I4_CHAIN
+                    const double2 rj = rjn;                 // r_kj (used by lanes j > k)
+                    if (k > 0) rjn = D[sw(k - 1, j)];
+#endif
                     if (k > 0) {
                         vn = D[sw(j, k - 1)];
 #pragma unroll
@@ -562,6 +570,7 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                         sa.x = fma(rk.x, xc[m].x, sa.x); sa.x = fma(-rk.y, xc[m].y, sa.x);
                         sa.y = fma(rk.x, xc[m].y, sa.y); sa.y = fma(rk.y, xc[m].x, sa.y);
                     }
+#ifdef HPDINV_DMMA_I4_CHAIN
                     if (j > k) {
                         xc[k] = make_double2(-ik * (s0.x + s1.x), -ik * (s0.y + s1.y));
                         if (lane < 8) D[sw(j, k)] = make_double2(xc[k].x, negd(xc[k].y));   // the mirror
@@ -581,6 +590,34 @@ k_dmma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                         }
                         xc[k] = make_double2(ik * (ik - (p + p2)), 0.0);
                     }
+#else
+                    // lane j > k forms x_kj and its own term Re(r_kj conj(x_kj)) of the x_kk sum;
+                    // the diagonal lane adds the terms pairwise (a tree of depth 3, not a chain)
+                    if (j > k) {
+                        xc[k] = make_double2(-ik * (s0.x + s1.x), -ik * (s0.y + s1.y));
+                        const double t = fma(rj.x, xc[k].x, rj.y * xc[k].y);
+                        if (lane < 8) {
+                            D[sw(j, k)] = make_double2(xc[k].x, negd(xc[k].y));     // the mirror
+                            tpart[j] = t;
+                        }
+                    }
+                    __syncwarp();
+                    if (j == k) {
+                        // x_kk = (1/r_kk)(1/r_kk - Re(V_kk + sum_{m>k} r_km conj(x_km)))
+                        double tt[8];
+#pragma unroll
+                        for (int m = 7; m > k; m--) {
+                            xc[m] = D[sw(m, k)];                                    // conj(x_km)
+                            tt[m] = tpart[m];
+                        }
+                        tt[k] = D[sw(k, k)].x;                                      // Re V_kk
+#pragma unroll
+                        for (int w = 1; w < 8; w *= 2)
+#pragma unroll
+                            for (int m = k; m + w <= 7; m += 2 * w) tt[m] += tt[m + w];
+                        xc[k] = make_double2(ik * (ik - tt[k]), 0.0);
+                    }
+#endif
                 }
                 __syncwarp();
                 if (lane < 8) {
