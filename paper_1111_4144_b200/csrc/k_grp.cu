@@ -35,6 +35,10 @@ static int launch_grp_t(const LaunchArgs& a) {
     // n >= 9 that fits in device memory does)
     if (!grp_strides_ok(a.sAe, a.sXe, sizeof(cplx<T>))) fn = nullptr;
     if (!fn) return kNoKernel;
+#ifndef HPDINV_GRP_NO_CONTIG
+    // contiguous matrices (sAe = sXe = 1, the AoS layout of cfg5): compile-time element offsets
+    if (a.n == 32 && a.sAe == 1 && a.sXe == 1) fn = k_grp<T, 32, 16, LDL, false, true>;
+#endif
 #ifndef HPDINV_GRP_NO_STAGE
     // staged global I/O (bulk copies of whole CTA plane segments, k_grp.cuh STG): interleaved A
     // and X with even plane strides and 16-byte aligned bases, n <= 16

@@ -131,7 +131,7 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned by
 // S1 + S2 of a lane group (shared by the inversion k_grp and the solve k_grp_solve): lane q
 // loads the upper part of its columns j = q + G*s and runs the right-looking factorisation with
 // the packed row store Rs; returns info.  See k_grp for the design notes.
-template <typename T, int N, int GG, bool LDL, bool STG = false>
+template <typename T, int N, int GG, bool LDL, bool STG = false, bool CONTIG = false>
 __device__ __forceinline__ int grp_factor(cplx<T> (&col)[GrpShape<T, N, GG>::C][N], const cplx<T>* __restrict__ Am,
                                           int64_t sAe, int q, cplx<T>* Rs, T* invs,
                                           const unsigned char* stq = nullptr) {
@@ -158,7 +158,8 @@ __device__ __forceinline__ int grp_factor(cplx<T> (&col)[GrpShape<T, N, GG>::C][
     } else {
         // element (l, j = q + G*s): lane base + (l*n + G*s) * plane stride; the plane stride in
         // bytes is < 2^32 (checked by the launcher), so each address is one IMAD.WIDE
-        const char* Ab = reinterpret_cast<const char*>(Am + q * sAe);
+        // (CONTIG: sAe = 1, every address is the lane base plus a compile-time offset)
+        const char* Ab = reinterpret_cast<const char*>(Am + q * (CONTIG ? 1 : sAe));
         const uint32_t seA = uint32_t(sAe * int64_t(sizeof(V)));
 #pragma unroll
         for (int s = 0; s < C; s++) {
@@ -167,7 +168,8 @@ __device__ __forceinline__ int grp_factor(cplx<T> (&col)[GrpShape<T, N, GG>::C][
             for (int l = 0; l < N; l++) {
                 col[s][l] = czero<T>();
                 if (l <= G * s + G - 1 && l <= j && j < N)
-                    col[s][l] = grp::ld(reinterpret_cast<const V*>(Ab + uint64_t(uint32_t(l * N + G * s)) * seA));
+                    col[s][l] = CONTIG ? grp::ld(reinterpret_cast<const V*>(Ab) + (l * N + G * s))
+                                       : grp::ld(reinterpret_cast<const V*>(Ab + uint64_t(uint32_t(l * N + G * s)) * seA));
             }
         }
     }
@@ -237,7 +239,7 @@ __device__ __forceinline__ int grp_factor(cplx<T> (&col)[GrpShape<T, N, GG>::C][
 // aligned bases -- checked by the launcher): a CTA holding MPC whole matrices moves its NUP
 // upper planes of A and its n^2 planes of X as bulk copies of MPC*ESZ bytes each through the
 // shared-memory staging area (GrpShape::SPS); a partial last CTA takes the per-lane path.
-template <typename T, int N, int GG, bool LDL, bool STG = false>
+template <typename T, int N, int GG, bool LDL, bool STG = false, bool CONTIG = false>
 __global__ void __launch_bounds__(GrpShape<T, N, GG>::THREADS, GrpShape<T, N, GG>::MIN_BLOCKS)
 k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
       cplx<T>* X, int64_t sXm, int64_t sXe, int32_t* __restrict__ info)
@@ -292,7 +294,7 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
 #endif
 
     V col[C][N];
-    int inf = grp_factor<T, N, GG, LDL, STG>(col, A + b * sAm, sAe, q, Rs, invs, stq);
+    int inf = grp_factor<T, N, GG, LDL, STG, CONTIG>(col, A + b * sAm, sAe, q, Rs, invs, stq);
 
     // ------------------------------------------------ S3/S4: proposed inversion, rows k = n..1
 #pragma unroll
@@ -395,7 +397,7 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
         // (storing each row as soon as it is final, inside S4, measured slower: 4.5 vs 4.1 ms cfg3)
         // every entry (m, j) is written once, by the owner of column j; a flagged matrix is
         // NaN-filled in the same store
-        char* Xrow = reinterpret_cast<char*>(X + b * sXm + q * sXe);   // element (m, q + G s)
+        char* Xrow = reinterpret_cast<char*>(X + b * sXm + q * (CONTIG ? 1 : sXe));   // element (m, q + G s)
         const uint32_t seX = uint32_t(sXe * int64_t(sizeof(V)));
         const T nan = qnan<T>();
 #pragma unroll
@@ -404,7 +406,8 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
             if (j < N) {
 #pragma unroll
                 for (int m = 0; m < N; m++)
-                    grp::st(reinterpret_cast<V*>(Xrow + uint64_t(uint32_t(m * N + G * s)) * seX),
+                    grp::st(CONTIG ? reinterpret_cast<V*>(Xrow) + (m * N + G * s)
+                                   : reinterpret_cast<V*>(Xrow + uint64_t(uint32_t(m * N + G * s)) * seX),
                             inf ? mk<T>(nan, nan) : col[s][m]);
             }
         }
