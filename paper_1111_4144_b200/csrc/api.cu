@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of include/hpdinv.h: argument validation, layout classification and
 // kernel-family selection per (method, dtype, n).  Host code only; the kernel families live
 // in their own translation units (k_reg.cu, k_lane_c64.cu, k_lane_c128.cu, k_generic.cu).
+#include <cstdlib>
 #include <mutex>
 #include <map>
 #include <utility>
@@ -28,7 +29,14 @@ cudaError_t ensure_smem(const void* fn, size_t bytes) {
     auto it = done.find({fn, dev});
     if (it != done.end() && it->second >= bytes) return cudaSuccess;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-    if (e == cudaSuccess) done[{fn, dev}] = bytes;
+    if (e != cudaSuccess) return e;
+    // tuning experiment: HPDINV_SMEM_CARVEOUT=<percent> sets the preferred shared-memory
+    // carveout of the large-smem kernels (unset: the driver's choice)
+    if (const char* cv = getenv("HPDINV_SMEM_CARVEOUT")) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
+        if (e != cudaSuccess) return e;
+    }
+    done[{fn, dev}] = bytes;
     return e;
 }
 
