@@ -76,7 +76,7 @@ static int launch_grp_solve_t(const SolveArgs& a) {
 #define HPDINV_GRPS(NN, GG)                         \
     case NN:                                        \
         fn = k_grp_solve<T, NN, GG, LDL>;           \
-        smem = GrpShape<T, NN, GG>::smem_bytes;     \
+        smem = GrpShape<T, NN, GG>::smem_bytes_full; \
         mpc = GrpShape<T, NN, GG>::MPC;             \
         threads = GrpShape<T, NN, GG>::THREADS;     \
         break;
