@@ -144,7 +144,7 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned by
 // S1 + S2 of a lane group (shared by the inversion k_grp and the solve k_grp_solve): lane q
 // loads the upper part of its columns j = q + G*s and runs the right-looking factorisation with
 // the packed row store Rs; returns info.  See k_grp for the design notes.
-template <typename T, int N, int GG, bool LDL, bool STG = false, bool CONTIG = false>
+template <typename T, int N, int GG, bool LDL, bool STG = false, bool CONTIG = false, bool INV_IN_ROW = false>
 __device__ __forceinline__ int grp_factor(cplx<T> (&col)[GrpShape<T, N, GG>::C][N], const cplx<T>* __restrict__ Am,
                                           int64_t sAe, int q, cplx<T>* Rs, T* invs,
                                           const unsigned char* stq = nullptr) {
@@ -206,8 +206,8 @@ __device__ __forceinline__ int grp_factor(cplx<T> (&col)[GrpShape<T, N, GG>::C][
         if (bad && inf == 0) inf = i + 1;
         V* Ri = Rs + Sh::roff(i);
         if (q == 0) {
-            if (invs) invs[i] = iv;
-            else reinterpret_cast<T*>(Ri)[0] = iv;      // COMPACT: Ri[0] is never a row entry
+            if constexpr (INV_IN_ROW) reinterpret_cast<T*>(Ri)[0] = iv;   // COMPACT: Ri[0] is never a row entry
+            else invs[i] = iv;
         }
         PMul<T> mul[C];
 #pragma unroll
@@ -310,7 +310,7 @@ k_grp(int64_t batch, const cplx<T>* __restrict__ A, int64_t sAm, int64_t sAe,
 #endif
 
     V col[C][N];
-    int inf = grp_factor<T, N, GG, LDL, STG, CONTIG>(col, A + b * sAm, sAe, q, Rs, invs, stq);
+    int inf = grp_factor<T, N, GG, LDL, STG, CONTIG, Sh::COMPACT>(col, A + b * sAm, sAe, q, Rs, invs, stq);
 
     // ------------------------------------------------ S3/S4: proposed inversion, rows k = n..1
 #pragma unroll
